@@ -1,0 +1,376 @@
+#!/usr/bin/env python3
+"""bench.py -- HEGrid hot path on B200: gridded samples x channels per second.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--impl ours|reference]
+
+One "step" = Eq. 1 for the whole workload (BASELINE.json configs[3] by default: 1M drift-scan
+samples x 4096 channels -> 300x300 map) on each rank's GPU: hegrid_grid_device on
+HBM-resident, plan-ordered channel-contiguous values (the layout the staging layer
+delivers), the plan (shared component, built once per coordinate set) prebuilt and its
+time reported separately.  Multi-GPU: one process per GPU (torchrun), channel shards,
+no data-path collective, weak scaling (each rank grids its own 4096 channels).
+
+Also measured in the same run:
+  e2e       -- the public host API (plan from host coords + hegrid_grid on pinned host
+               [C][N] values -> pinned host maps), H2D/D2H inside the timed region;
+  roofline  -- the accumulate kernel (the dominant kernel) timed with CUDA events on its
+               launch stream; binding roof = FP32 FMA issue (alu), plus the north_star's
+               HBM-roofline fraction;
+  cpu_baseline -- the fp64 oracle on this host's cores, on a bounded sample of cells.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "gridded samples x channels per second"
+UNIT = "samples*channels/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            if self.thread:
+                self.thread.join(timeout=2)
+        return self.summary()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "power_w_max": max(pw) if pw else None,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def plan_layout_values(w, lon, lat, perm, channel_ids, device):
+    """Values of the given channels, generated directly in plan order [n_used][C]."""
+    C = len(channel_ids)
+    out = torch.empty((perm.shape[0], C), dtype=torch.float32, device=device)
+    ch = torch.as_tensor(channel_ids, dtype=torch.int64, device=device)
+    for c0 in range(0, C, 256):
+        blk = synth.values(w, lon, lat, channels=ch[c0:c0 + 256], samples=perm)
+        out[:, c0:c0 + blk.shape[0]] = blk.t()
+        del blk
+    return out
+
+
+def user_layout_values_pinned(w, lon, lat, channel_ids, device):
+    """Values [C][N] in original sample order in pinned host memory (the e2e input)."""
+    C, N = len(channel_ids), lon.shape[0]
+    host = torch.empty((C, N), dtype=torch.float32, pin_memory=True)
+    ch = torch.as_tensor(channel_ids, dtype=torch.int64, device=device)
+    for c0 in range(0, C, 256):
+        host[c0:c0 + 256].copy_(synth.values(w, lon, lat, channels=ch[c0:c0 + 256]).cpu())
+    return host
+
+
+def oracle_sample(w, lon_h, lat_h, vals_h, target_s=12.0, max_cells=None):
+    """Time the fp64 oracle (all host cores) on an evenly spaced sample of cells with all
+    channels; return (throughput samples*ch/s extrapolated to the whole map, detail)."""
+    import oracle
+    oracle.build()
+    nthreads = oracle.max_threads()
+    cells_all = w.cells
+    # calibration round: one cell per thread
+    k = min(nthreads, cells_all)
+    cal = np.linspace(0, cells_all - 1, k).astype(np.int64)
+    t0 = time.perf_counter()
+    oracle.grid(lon_h, lat_h, vals_h, w.map, w.fwhm_deg, w.support, cells=cal, nthreads=nthreads)
+    t_cal = time.perf_counter() - t0
+    n_cells = int(max(k, min(cells_all, k * max(1.0, target_s / max(t_cal, 1e-3)))))
+    if max_cells:
+        n_cells = min(n_cells, max_cells)
+    cells = np.linspace(0, cells_all - 1, n_cells).astype(np.int64)
+    t0 = time.perf_counter()
+    oracle.grid(lon_h, lat_h, vals_h, w.map, w.fwhm_deg, w.support, cells=cells, nthreads=nthreads)
+    t = time.perf_counter() - t0
+    thr = w.n * vals_h.shape[0] * (n_cells / cells_all) / t
+    return thr, {"cores": nthreads, "cells": n_cells, "seconds": t,
+                 "sample": f"{n_cells} of {cells_all} cells (evenly spaced) x all "
+                           f"{vals_h.shape[0]} channels x all {w.n} samples, fp64 brute force; "
+                           f"throughput scaled by cells_all/{n_cells}"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, on this host's cores, same metric/config."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    w = synth.CONFIGS[args.workload]
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    lon, lat = synth.coords(w, device=dev)
+    C = w.channels
+    vals = torch.empty((C, w.n), dtype=torch.float32)
+    ch = torch.arange(C, device=dev)
+    for c0 in range(0, C, 256):
+        vals[c0:c0 + 256] = synth.values(w, lon, lat, channels=ch[c0:c0 + 256]).cpu()
+    lon_h, lat_h, vals_h = lon.cpu().numpy(), lat.cpu().numpy(), vals.numpy()
+    budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
+    per = []
+    detail = None
+    for s in range(args.warmup + args.steps):
+        thr, detail = oracle_sample(w, lon_h, lat_h, vals_h, target_s=budget)
+        if s >= args.warmup:
+            per.append(w.n * C / thr)     # seconds for one whole-workload step (extrapolated)
+    ms = 1000 * statistics.median(per)
+    value = w.n * C / (ms / 1000)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(w, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": detail["cores"],
+                             "kind": "oracle", "sample": detail["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(w, world):
+    return {"workload": w.name, "desc": w.note, "n_samples": w.n, "channels_per_gpu": w.channels,
+            "global_channels": w.channels * world, "map": f"{w.nx}x{w.ny}",
+            "cell_deg": w.cdelt, "kernel_fwhm_deg": w.fwhm_deg, "support_sigma": w.support,
+            "field_deg": [w.field_lon, w.field_lat], "centre_deg": list(w.centre),
+            "sampling": w.kind, "parallelism": f"channel-shard x{world}",
+            "input_layout": "plan-ordered [n_used][C] fp32, HBM-resident",
+            "l2": "inputs larger than L2 (values %.1f GB vs 126 MB L2)" % (w.n * w.channels * 4 / 1e9)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="cfg4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", local)
+    from paper_2207_04584_b200 import Plan, abi
+
+    w = synth.CONFIGS[args.workload]
+    C = w.channels
+    channel_ids = list(range(rank * C, (rank + 1) * C))      # weak scaling: own shard
+    lon, lat = synth.coords(w, device=dev)
+
+    # ---------------------------------------------------------------- plan (once)
+    stream = torch.cuda.current_stream(dev)
+    plan = Plan(lon, lat, w.map, w.fwhm_deg, w.support, device=local, stream=stream)
+    info = plan.info()
+    perm = torch.as_tensor(plan.permutation(), device=dev)
+    vp = plan_layout_values(w, lon, lat, perm, channel_ids, dev)
+    out = torch.empty((C, w.ny, w.nx), dtype=torch.float32, device=dev)
+    Wmap = torch.empty((w.ny, w.nx), dtype=torch.float32, device=dev)
+    torch.cuda.synchronize(dev)
+
+    def step():
+        plan.grid_plan_layout(vp, C, out, Wmap, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    plan.profile(True)
+    plan.profile_read()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = abi.hegrid_launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = abi.hegrid_launch_count() - l0
+    clk = clocks.stop()
+    ms_total = e0.elapsed_time(e1)
+    k_ms, k_n = plan.profile_read()
+    plan.profile(False)
+    t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    units = w.n * C * world
+    value = units / (ms_step / 1000)
+
+    # ---------------------------------------------------------------- roofline
+    peaks, peak_src = load_peaks()
+    k_avg_ms = k_ms / max(k_n, 1)
+    cells = w.cells
+    alg_bytes = (4 * info["n_used"] * C + 4 * cells * C + 4 * cells + 16 * info["n_used"]
+                 + 4 * (info["n_bins"] + 1))
+    flops = 2.0 * info["n_pairs"] * C
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak_tflops = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    hbm_achieved = alg_bytes / (k_avg_ms / 1000) / 1e9
+    alu_achieved = flops / (k_avg_ms / 1000) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(w.name, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roof = {"bound": "alu", "achieved": alu_achieved, "peak": fp32_peak_tflops, "unit": "TFLOP/s",
+            "frac": alu_achieved / fp32_peak_tflops, "traffic": traffic,
+            "kernel": "k_accum_simt", "kernel_ms": k_avg_ms, "kernel_share": k_ms / ms_total if ms_total else None,
+            "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": alg_bytes,
+            "peak_source": "148 SMs x 128 FP32 lanes x 2 flop x sm_max_mhz (DESIGN.md)"}
+    hbm_roof = {"achieved": hbm_achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": hbm_achieved / peaks["hbm_gbs"], "peak_source": f"{peak_src} hbm_gbs",
+                "step_frac": (alg_bytes / (ms_step / 1000) / 1e9) / peaks["hbm_gbs"]}
+
+    # ---------------------------------------------------------------- e2e (public host API)
+    e2e = None
+    host_vals = None
+    if not args.no_e2e:
+        del vp
+        torch.cuda.empty_cache()
+        host_vals = user_layout_values_pinned(w, lon, lat, channel_ids, dev)
+        host_out = torch.empty((C, w.ny, w.nx), dtype=torch.float32, pin_memory=True)
+        host_w = torch.empty((w.ny, w.nx), dtype=torch.float32, pin_memory=True)
+        lon_h = lon.cpu().numpy()
+        lat_h = lat.cpu().numpy()
+
+        def e2e_step():
+            with Plan(lon_h, lat_h, w.map, w.fwhm_deg, w.support, device=local) as p:
+                p.grid(host_vals, host_out, host_w)
+            return float(host_w[w.ny // 2, w.nx // 2])   # read of the result
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        te = (time.perf_counter() - t0) / args.e2e_steps
+        tt = torch.tensor([te], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+        e2e = {"value": units / te, "unit": UNIT, "ms_per_step": te * 1000,
+               "h2d_bytes_per_step": C * w.n * 4 + 16 * w.n,
+               "d2h_bytes_per_step": C * cells * 4 + cells * 4,
+               "api": "Plan(host coords) + hegrid_grid(pinned host [C][N] -> pinned host maps)"}
+
+    # ---------------------------------------------------------------- cpu baseline (rank 0, N=1)
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        if host_vals is None:
+            host_vals = user_layout_values_pinned(w, lon, lat, channel_ids, dev)
+        thr, det = oracle_sample(w, lon.cpu().numpy(), lat.cpu().numpy(), host_vals.numpy())
+        cpu = {"value": thr, "unit": UNIT, "cores": det["cores"], "kind": "oracle",
+               "sample": det["sample"], "seconds": det["seconds"]}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic (seeded drift-scan coords, sky-model values)",
+                "config": workload_config(w, world),
+                "plan_ms": info["t_plan_ms"],
+                "pairs": {"n_pairs": info["n_pairs"], "candidates": info["n_candidate_pairs"],
+                          "nbr_mean": info["nbr_mean"]},
+                "roofline": roof, "hbm_roofline": hbm_roof, "clocks": clk,
+                "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

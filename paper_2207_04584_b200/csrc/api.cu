@@ -1,0 +1,447 @@
+// api.cu -- the C ABI (include/hegrid.h): validation, plan lifetime, the device-resident
+// grid call, and the host end-to-end pipeline (channel blocks over CUDA streams with
+// pinned staging; PAPER.md:279-294 multi-pipeline concurrency, :313-318 memory pool,
+// pinned memory and asynchronous transfer).
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+
+namespace hg {
+std::atomic<int64_t> g_launches{0};
+
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        err = cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+static bool is_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+static void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+    const size_t chunk = 64ull << 20;
+    int nt = (int)std::min<size_t>(std::max<size_t>(bytes / chunk, 1), 16);
+    if (nt <= 1) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> th;
+    size_t per = (bytes + nt - 1) / nt;
+    for (int t = 0; t < nt; ++t) {
+        size_t b = t * per, e = std::min(bytes, b + per);
+        if (b >= e) break;
+        th.emplace_back([=] { memcpy((char*)dst + b, (const char*)src + b, e - b); });
+    }
+    for (auto& x : th) x.join();
+}
+
+static hegrid_status validate_geometry(const hegrid_map* m, const hegrid_kernel* k) {
+    if (!m || !k) return HEGRID_EINVAL;
+    if (m->nx < 1 || m->ny < 1) return HEGRID_EINVAL;
+    if ((int64_t)m->nx * m->ny > (1LL << 31)) return HEGRID_EINVAL;
+    const double v[] = {m->crval_lon, m->crval_lat, m->crpix_x, m->crpix_y, m->cdelt_lon,
+                        m->cdelt_lat, k->fwhm_deg, k->support_sigma};
+    for (double x : v)
+        if (!isfinite(x)) return HEGRID_EINVAL;
+    if (m->cdelt_lon == 0.0 || m->cdelt_lat == 0.0) return HEGRID_EINVAL;
+    if (!(k->fwhm_deg > 0.0) || !(k->support_sigma > 0.0)) return HEGRID_EINVAL;
+    if (fabs(m->crval_lat) > 90.0) return HEGRID_EINVAL;
+    return HEGRID_OK;
+}
+
+static hegrid_opts default_opts(const hegrid_opts* o) {
+    hegrid_opts r{};
+    if (o) r = *o;
+    if (r.n_streams <= 0) r.n_streams = 2;
+    if (r.n_streams > 8) r.n_streams = 8;
+    if (r.channel_block < 0) r.channel_block = 0;
+    return r;
+}
+
+static hegrid_status create_common(const double* d_lon, const double* d_lat, int64_t n,
+                                   const hegrid_map* map, const hegrid_kernel* kernel,
+                                   const hegrid_opts& o, cudaStream_t st, hegrid_plan_t* out) {
+    auto* p = new (std::nothrow) hegrid_plan_s();
+    if (!p) return HEGRID_ENOMEM;
+    p->device = o.device;
+    p->map = *map;
+    p->kern = *kernel;
+    p->opts = o;
+    p->n = n;
+    hegrid_status s = build_plan(p, d_lon, d_lat, st);
+    if (s != HEGRID_OK) {
+        hegrid_plan_destroy(p);
+        return s;
+    }
+    *out = p;
+    return HEGRID_OK;
+}
+
+}  // namespace hg
+
+using namespace hg;
+
+extern "C" {
+
+const char* hegrid_status_string(hegrid_status s) {
+    switch (s) {
+        case HEGRID_OK: return "ok";
+        case HEGRID_EINVAL: return "invalid argument";
+        case HEGRID_EDOMAIN: return "sample coordinate out of domain (non-finite or |lat| > 90)";
+        case HEGRID_ENOMEM: return "out of memory";
+        case HEGRID_ECUDA: return "CUDA error or no usable device";
+        case HEGRID_EUNSUPPORTED: return "geometry not supported by the lon/lat bin index";
+        case HEGRID_EINTERNAL: return "internal error";
+    }
+    return "unknown status";
+}
+
+int32_t hegrid_abi_version(void) { return HEGRID_ABI_VERSION; }
+
+int64_t hegrid_launch_count(void) { return g_launches.load(); }
+
+hegrid_status hegrid_plan_create(const double* lon_deg, const double* lat_deg, int64_t n,
+                                 const hegrid_map* map, const hegrid_kernel* kernel,
+                                 const hegrid_opts* opts, hegrid_plan_t* out) {
+    if (!out || n < 0 || n >= (1LL << 31) - 1) return HEGRID_EINVAL;
+    if (n > 0 && (!lon_deg || !lat_deg)) return HEGRID_EINVAL;
+    HG_TRY_S(validate_geometry(map, kernel));
+    hegrid_opts o = default_opts(opts);
+    DeviceGuard dg(o.device);
+    HG_TRY(dg.err);
+    double *d_lon = nullptr, *d_lat = nullptr;
+    size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(double);
+    HG_TRY(cudaMalloc(&d_lon, bytes));
+    cudaError_t e = cudaMalloc(&d_lat, bytes);
+    if (e == cudaSuccess && n > 0) e = cudaMemcpy(d_lon, lon_deg, n * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && n > 0) e = cudaMemcpy(d_lat, lat_deg, n * 8, cudaMemcpyHostToDevice);
+    hegrid_status s = cuda_status(e);
+    if (s == HEGRID_OK) s = create_common(d_lon, d_lat, n, map, kernel, o, 0, out);
+    cudaFree(d_lon);
+    if (d_lat) cudaFree(d_lat);
+    return s;
+}
+
+hegrid_status hegrid_plan_create_device(const double* d_lon, const double* d_lat, int64_t n,
+                                        const hegrid_map* map, const hegrid_kernel* kernel,
+                                        const hegrid_opts* opts, void* stream,
+                                        hegrid_plan_t* out) {
+    if (!out || n < 0 || n >= (1LL << 31) - 1) return HEGRID_EINVAL;
+    if (n > 0 && (!d_lon || !d_lat)) return HEGRID_EINVAL;
+    HG_TRY_S(validate_geometry(map, kernel));
+    hegrid_opts o = default_opts(opts);
+    DeviceGuard dg(o.device);
+    HG_TRY(dg.err);
+    return create_common(d_lon, d_lat, n, map, kernel, o, (cudaStream_t)stream, out);
+}
+
+void hegrid_plan_destroy(hegrid_plan_t p) {
+    if (!p) return;
+    DeviceGuard dg(p->device);
+    cudaFree(p->d_keys);
+    cudaFree(p->d_perm);
+    cudaFree(p->d_iperm);
+    cudaFree(p->d_geo);
+    cudaFree(p->d_ll);
+    cudaFree(p->d_bin_start);
+    cudaFree(p->d_mrow);
+    cudaFree(p->d_cos_row);
+    cudaFree(p->d_scratch);
+    for (auto e : p->prof_events) cudaEventDestroy(e);
+    delete p;
+}
+
+hegrid_status hegrid_plan_info(hegrid_plan_t p, hegrid_plan_stats* out) {
+    if (!p || !out) return HEGRID_EINVAL;
+    DeviceGuard dg(p->device);
+    HG_TRY(dg.err);
+    if (!p->stats_valid) {
+        HG_TRY_S(plan_pair_stats(p, 0));
+        p->stats_valid = true;
+    }
+    hegrid_plan_stats s = p->stats;
+    s.n_samples = p->n;
+    s.n_used = p->n_used;
+    s.n_bins = p->g.nbins;
+    s.t_plan_ms = p->t_plan_ms;
+    s.nrow = p->g.nrow;
+    s.ncol = p->g.ncol;
+    s.mlat = p->g.mlat;
+    s.mlon = p->g.mlon;
+    s.sigma_deg = p->g.sigma_rad / kDeg2Rad;
+    s.radius_deg = p->g.R_rad / kDeg2Rad;
+    *out = s;
+    return HEGRID_OK;
+}
+
+hegrid_status hegrid_plan_permutation(hegrid_plan_t p, int64_t* perm, int64_t* n_used) {
+    if (!p) return HEGRID_EINVAL;
+    if (n_used) *n_used = p->n_used;
+    if (!perm || p->n_used == 0) return HEGRID_OK;
+    DeviceGuard dg(p->device);
+    HG_TRY(dg.err);
+    std::vector<int32_t> h(p->n_used);
+    HG_TRY(cudaMemcpy(h.data(), p->d_perm, p->n_used * 4, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < p->n_used; ++i) perm[i] = h[i];
+    return HEGRID_OK;
+}
+
+hegrid_status hegrid_permute_device(hegrid_plan_t p, const float* d_user, int64_t n_channels,
+                                    int64_t ld_user, float* d_plan, int64_t ld_plan,
+                                    void* stream) {
+    if (!p || n_channels < 0) return HEGRID_EINVAL;
+    if (n_channels == 0) return HEGRID_OK;
+    if (!d_user || !d_plan || ld_user < p->n || ld_plan < n_channels || ld_plan % 4) return HEGRID_EINVAL;
+    DeviceGuard dg(p->device);
+    HG_TRY(dg.err);
+    return launch_permute(p, d_user, n_channels, ld_user, d_plan, ld_plan, (cudaStream_t)stream);
+}
+
+static hegrid_status accumulate_profiled(hegrid_plan_s* p, const float* d_v, int64_t ldv,
+                                         int64_t C, float* d_out, float* d_w, cudaStream_t st) {
+    if (!p->profile) return launch_accumulate_simt(p, d_v, ldv, C, d_out, d_w, st);
+    cudaEvent_t a, b;
+    HG_TRY(cudaEventCreate(&a));
+    HG_TRY(cudaEventCreate(&b));
+    HG_TRY(cudaEventRecord(a, st));
+    hegrid_status s = launch_accumulate_simt(p, d_v, ldv, C, d_out, d_w, st);
+    HG_TRY(cudaEventRecord(b, st));
+    p->prof_events.push_back(a);
+    p->prof_events.push_back(b);
+    return s;
+}
+
+// W only (n_channels == 0 but a weight map was requested): one pass over a zero row.
+static hegrid_status weights_only(hegrid_plan_s* p, float* d_w, cudaStream_t st) {
+    float* z = nullptr;
+    float* o = nullptr;
+    size_t nz = (size_t)std::max<int64_t>(p->n_used, 1) * 4;
+    HG_TRY(cudaMallocAsync(&z, nz * sizeof(float), st));
+    HG_TRY(cudaMallocAsync(&o, (size_t)p->g.nx * p->g.ny * sizeof(float), st));
+    HG_TRY(cudaMemsetAsync(z, 0, nz * sizeof(float), st));
+    hegrid_status s = launch_accumulate_simt(p, z, 4, 1, o, d_w, st);
+    cudaFreeAsync(z, st);
+    cudaFreeAsync(o, st);
+    return s;
+}
+
+hegrid_status hegrid_grid_device(hegrid_plan_t p, const float* d_data, int64_t n_channels,
+                                 int64_t ld, int32_t layout, float* d_out, float* d_weight,
+                                 void* stream) {
+    if (!p || n_channels < 0) return HEGRID_EINVAL;
+    if (n_channels > 0 && (!d_data || !d_out)) return HEGRID_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    DeviceGuard dg(p->device);
+    HG_TRY(dg.err);
+    if (n_channels == 0) return d_weight ? weights_only(p, d_weight, st) : HEGRID_OK;
+    const int64_t cells = (int64_t)p->g.nx * p->g.ny;
+    if (layout == HEGRID_LAYOUT_PLAN_NC) {
+        if (ld < n_channels || ld % 4 || ((uintptr_t)d_data & 15)) return HEGRID_EINVAL;
+        return accumulate_profiled(p, d_data, ld, n_channels, d_out, d_weight, st);
+    }
+    if (layout != HEGRID_LAYOUT_USER_CN) return HEGRID_EINVAL;
+    if (ld < p->n) return HEGRID_EINVAL;
+    // USER_CN: permute channel blocks through a plan-layout scratch
+    int64_t cb = std::min<int64_t>(n_channels, 512);
+    cb = (cb + 3) & ~3LL;
+    size_t need = (size_t)std::max<int64_t>(p->n_used, 1) * cb * sizeof(float);
+    if (p->scratch_bytes < need) {
+        cudaFree(p->d_scratch);
+        p->d_scratch = nullptr;
+        p->scratch_bytes = 0;
+        HG_TRY(cudaMalloc(&p->d_scratch, need));
+        p->scratch_bytes = need;
+    }
+    for (int64_t c0 = 0; c0 < n_channels; c0 += cb) {
+        int64_t cn = std::min(cb, n_channels - c0);
+        HG_TRY_S(launch_permute(p, d_data + c0 * ld, cn, ld, p->d_scratch, cb, st));
+        HG_TRY_S(accumulate_profiled(p, p->d_scratch, cb, cn, d_out + c0 * cells,
+                                     c0 == 0 ? d_weight : nullptr, st));
+    }
+    return HEGRID_OK;
+}
+
+hegrid_status hegrid_grid(hegrid_plan_t p, const float* data, int64_t n_channels,
+                          float* out_map, float* weight_map) {
+    if (!p || n_channels < 0) return HEGRID_EINVAL;
+    if (n_channels > 0 && (!out_map || (p->n > 0 && !data))) return HEGRID_EINVAL;
+    DeviceGuard dg(p->device);
+    HG_TRY(dg.err);
+    const int64_t cells = (int64_t)p->g.nx * p->g.ny;
+    const int64_t n = p->n;
+    float* d_w = nullptr;
+    if (weight_map) HG_TRY(cudaMalloc(&d_w, cells * sizeof(float)));
+    if (n_channels == 0) {
+        hegrid_status s = HEGRID_OK;
+        if (weight_map) {
+            s = weights_only(p, d_w, 0);
+            if (s == HEGRID_OK)
+                s = cuda_status(cudaMemcpy(weight_map, d_w, cells * 4, cudaMemcpyDeviceToHost));
+            cudaFree(d_w);
+        }
+        return s;
+    }
+    int64_t cb = p->opts.channel_block > 0 ? p->opts.channel_block
+                                           : (n_channels >= 1024 ? 512 : 256);
+    cb = std::min<int64_t>(cb, n_channels);
+    cb = (cb + 3) & ~3LL;
+    const int S = p->opts.n_streams;
+    const int64_t nblk = (n_channels + cb - 1) / cb;
+    const bool in_pinned = n == 0 || is_pinned(data);
+    const bool out_pinned = is_pinned(out_map);
+    struct Slot {
+        cudaStream_t st = nullptr;
+        cudaEvent_t done = nullptr;
+        float *d_raw = nullptr, *d_v = nullptr, *d_out = nullptr;
+        float *h_in = nullptr, *h_out = nullptr;
+        int64_t pending = -1;   // block whose output waits in h_out
+    };
+    std::vector<Slot> sl(S);
+    hegrid_status s = HEGRID_OK;
+    auto fail = [&](cudaError_t e) {
+        if (s == HEGRID_OK && e != cudaSuccess) s = cuda_status(e);
+        return s != HEGRID_OK;
+    };
+    const size_t raw_b = (size_t)cb * std::max<int64_t>(n, 1) * 4;
+    const size_t v_b = (size_t)cb * std::max<int64_t>(p->n_used, 1) * 4;
+    const size_t out_b = (size_t)cb * cells * 4;
+    for (int k = 0; k < S && s == HEGRID_OK; ++k) {
+        if (fail(cudaStreamCreateWithFlags(&sl[k].st, cudaStreamNonBlocking))) break;
+        if (fail(cudaEventCreateWithFlags(&sl[k].done, cudaEventDisableTiming))) break;
+        if (fail(cudaMalloc(&sl[k].d_raw, raw_b))) break;
+        if (fail(cudaMalloc(&sl[k].d_v, v_b))) break;
+        if (fail(cudaMalloc(&sl[k].d_out, out_b))) break;
+        if (!in_pinned && fail(cudaHostAlloc(&sl[k].h_in, raw_b, cudaHostAllocDefault))) break;
+        if (!out_pinned && fail(cudaHostAlloc(&sl[k].h_out, out_b, cudaHostAllocDefault))) break;
+    }
+    auto drain = [&](Slot& x) {
+        if (x.pending < 0) return;
+        if (fail(cudaEventSynchronize(x.done))) return;
+        if (!out_pinned) {
+            int64_t c0 = x.pending * cb, cn = std::min(cb, n_channels - c0);
+            parallel_memcpy(out_map + c0 * cells, x.h_out, (size_t)cn * cells * 4);
+        }
+        x.pending = -1;
+    };
+    for (int64_t b = 0; b < nblk && s == HEGRID_OK; ++b) {
+        Slot& x = sl[b % S];
+        drain(x);
+        if (s != HEGRID_OK) break;
+        const int64_t c0 = b * cb, cn = std::min(cb, n_channels - c0);
+        if (n > 0) {
+            const float* src = data + c0 * n;
+            if (!in_pinned) {
+                parallel_memcpy(x.h_in, src, (size_t)cn * n * 4);
+                src = x.h_in;
+            }
+            if (fail(cudaMemcpyAsync(x.d_raw, src, (size_t)cn * n * 4, cudaMemcpyHostToDevice,
+                                     x.st)))
+                break;
+            if ((s = launch_permute(p, x.d_raw, cn, n, x.d_v, cb, x.st)) != HEGRID_OK) break;
+        }
+        if ((s = launch_accumulate_simt(p, x.d_v, cb, cn, x.d_out, b == 0 ? d_w : nullptr,
+                                        x.st)) != HEGRID_OK)
+            break;
+        float* dst = out_pinned ? out_map + c0 * cells : x.h_out;
+        if (fail(cudaMemcpyAsync(dst, x.d_out, (size_t)cn * cells * 4, cudaMemcpyDeviceToHost,
+                                 x.st)))
+            break;
+        if (fail(cudaEventRecord(x.done, x.st))) break;
+        x.pending = b;
+    }
+    for (auto& x : sl) drain(x);
+    if (s == HEGRID_OK && weight_map) {
+        fail(cudaStreamSynchronize(sl[0].st));
+        if (s == HEGRID_OK) fail(cudaMemcpy(weight_map, d_w, cells * 4, cudaMemcpyDeviceToHost));
+    }
+    for (auto& x : sl) {
+        if (x.st) cudaStreamSynchronize(x.st);
+        cudaFree(x.d_raw);
+        cudaFree(x.d_v);
+        cudaFree(x.d_out);
+        if (x.h_in) cudaFreeHost(x.h_in);
+        if (x.h_out) cudaFreeHost(x.h_out);
+        if (x.done) cudaEventDestroy(x.done);
+        if (x.st) cudaStreamDestroy(x.st);
+    }
+    if (d_w) cudaFree(d_w);
+    return s;
+}
+
+hegrid_status hegrid_neighbours(hegrid_plan_t p, int64_t cell_begin, int64_t cell_end,
+                                int64_t* offsets, int64_t* sample_idx) {
+    if (!p || !offsets) return HEGRID_EINVAL;
+    int64_t cells = (int64_t)p->g.nx * p->g.ny;
+    if (cell_begin < 0 || cell_end < cell_begin || cell_end > cells) return HEGRID_EINVAL;
+    DeviceGuard dg(p->device);
+    HG_TRY(dg.err);
+    return plan_neighbours(p, cell_begin, cell_end, offsets, sample_idx, 0);
+}
+
+hegrid_status hegrid_sort_u32(const uint32_t* keys, int64_t n, int32_t* perm, int32_t device) {
+    if (n < 0 || n >= (1LL << 31) - 1 || (n > 0 && (!keys || !perm))) return HEGRID_EINVAL;
+    if (n == 0) return HEGRID_OK;
+    DeviceGuard dg(device);
+    HG_TRY(dg.err);
+    uint32_t* dk = nullptr;
+    int32_t* dv = nullptr;
+    std::vector<int32_t> iota(n);
+    for (int64_t i = 0; i < n; ++i) iota[i] = (int32_t)i;
+    HG_TRY(cudaMalloc(&dk, n * 4));
+    cudaError_t e = cudaMalloc(&dv, n * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(dk, keys, n * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dv, iota.data(), n * 4, cudaMemcpyHostToDevice);
+    hegrid_status s = cuda_status(e);
+    if (s == HEGRID_OK) s = radix_sort_pairs(dk, dv, n, 32, 0);
+    if (s == HEGRID_OK) s = cuda_status(cudaMemcpy(perm, dv, n * 4, cudaMemcpyDeviceToHost));
+    cudaFree(dk);
+    if (dv) cudaFree(dv);
+    return s;
+}
+
+hegrid_status hegrid_profile_enable(hegrid_plan_t p, int32_t enable) {
+    if (!p) return HEGRID_EINVAL;
+    p->profile = enable != 0;
+    return HEGRID_OK;
+}
+
+hegrid_status hegrid_profile_read(hegrid_plan_t p, double* ms, int64_t* launches) {
+    if (!p) return HEGRID_EINVAL;
+    DeviceGuard dg(p->device);
+    HG_TRY(dg.err);
+    double tot = 0;
+    int64_t k = 0;
+    hegrid_status s = HEGRID_OK;
+    for (size_t i = 0; i + 1 < p->prof_events.size(); i += 2) {
+        float x = 0;
+        cudaError_t e = cudaEventSynchronize(p->prof_events[i + 1]);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&x, p->prof_events[i], p->prof_events[i + 1]);
+        if (e != cudaSuccess) s = cuda_status(e);
+        tot += x;
+        ++k;
+    }
+    for (auto e : p->prof_events) cudaEventDestroy(e);
+    p->prof_events.clear();
+    if (ms) *ms = tot;
+    if (launches) *launches = k;
+    return s;
+}
+
+}  // extern "C"

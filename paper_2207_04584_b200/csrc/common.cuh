@@ -1,0 +1,119 @@
+// common.cuh -- internal types shared by the hegrid CUDA translation units.
+// Nothing here is part of the ABI (include/hegrid.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <vector>
+
+#include "../../include/hegrid.h"
+
+namespace hg {
+
+extern std::atomic<int64_t> g_launches;
+inline void count_launch(int k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kDeg2Rad = kPi / 180.0;
+
+// Geometry of the bin index and kernel, passed by value to kernels.
+// Bin (br, bc) of the index covers the cell-sized box around cell (bc - mlon, br - mlat);
+// the bin grid is nrow x ncol = (ny + 2 mlat) x (nx + 2 mlon); key = br * ncol + bc,
+// samples that cannot reach any cell get key = nbins (sorted to the end, never read).
+struct Geom {
+    int nx, ny;
+    int nrow, ncol, mlat, mlon;
+    int rl;                 // bin-row reach of a cell row (rows j-rl .. j+rl)
+    int64_t nbins;
+    // fp64 map header (cell centres, fp64 recheck)
+    double crval_lon, crval_lat, crpix_x, crpix_y, cdelt_lon, cdelt_lat;
+    double R_rad, sigma_rad;
+    // fp32 constants of the hot-path weight
+    float dlon_rad, dlat_rad;   // cdelt in radians (signed)
+    float R2_lo, R2_hi;         // guard band around R^2 (rad^2): below -> in, above -> out
+    float neg_k2;               // -log2(e) / (2 sigma^2)  (w = 2^(d^2 * neg_k2))
+};
+
+// Per-sample plan data in plan order.
+// geo = { x offset from bin centre (cells), y offset (cells), cos(lat), bin column (as int bits) }
+struct PlanDev {
+    const float4* geo;
+    const double2* ll;          // fp64 (lon, lat) deg, plan order (guard-band recheck)
+    const uint32_t* bin_start;  // [nbins + 1]
+    const int* mrow;            // [nrow] lon reach (bins) of a cell for samples in that bin row
+    const float* cos_row;       // [ny] cos(lat) of cell rows (fp32)
+};
+
+}  // namespace hg
+
+struct hegrid_plan_s {
+    int device = 0;
+    hegrid_map map{};
+    hegrid_kernel kern{};
+    hegrid_opts opts{};
+    int64_t n = 0, n_used = 0;
+    hg::Geom g{};
+    // device arrays
+    uint32_t* d_keys = nullptr;     // sorted keys [n]
+    int32_t* d_perm = nullptr;      // plan position -> original index [n]
+    int32_t* d_iperm = nullptr;     // original index -> plan position [n]
+    float4* d_geo = nullptr;        // [n_used]
+    double2* d_ll = nullptr;        // [n_used]
+    uint32_t* d_bin_start = nullptr;
+    int* d_mrow = nullptr;
+    float* d_cos_row = nullptr;
+    double t_plan_ms = 0;
+    bool stats_valid = false;
+    hegrid_plan_stats stats{};
+    // profiling
+    bool profile = false;
+    std::vector<cudaEvent_t> prof_events;  // start/stop pairs
+    // scratch for USER_CN device grids
+    float* d_scratch = nullptr;
+    size_t scratch_bytes = 0;
+
+    hg::PlanDev dev() const {
+        return hg::PlanDev{d_geo, d_ll, d_bin_start, d_mrow, d_cos_row};
+    }
+};
+
+namespace hg {
+
+// plan.cu
+hegrid_status build_plan(hegrid_plan_s* p, const double* d_lon, const double* d_lat,
+                         cudaStream_t st);
+hegrid_status radix_sort_pairs(uint32_t* d_keys, int32_t* d_vals, int64_t n, int bits,
+                               cudaStream_t st);
+hegrid_status plan_pair_stats(hegrid_plan_s* p, cudaStream_t st);
+hegrid_status plan_neighbours(hegrid_plan_s* p, int64_t c0, int64_t c1, int64_t* offsets,
+                              int64_t* idx, cudaStream_t st);
+
+// grid_simt.cu
+hegrid_status launch_accumulate_simt(const hegrid_plan_s* p, const float* d_v, int64_t ldv,
+                                     int64_t n_channels, float* d_out, float* d_weight,
+                                     cudaStream_t st);
+// permute.cu
+hegrid_status launch_permute(const hegrid_plan_s* p, const float* d_user, int64_t n_channels,
+                             int64_t ld_user, float* d_plan, int64_t ld_plan, cudaStream_t st);
+
+inline hegrid_status cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return HEGRID_OK;
+    if (e == cudaErrorMemoryAllocation) return HEGRID_ENOMEM;
+    return HEGRID_ECUDA;
+}
+
+}  // namespace hg
+
+#define HG_TRY(expr)                                         \
+    do {                                                     \
+        cudaError_t _e = (expr);                             \
+        if (_e != cudaSuccess) return hg::cuda_status(_e);   \
+    } while (0)
+
+#define HG_TRY_S(expr)                      \
+    do {                                    \
+        hegrid_status _s = (expr);          \
+        if (_s != HEGRID_OK) return _s;     \
+    } while (0)

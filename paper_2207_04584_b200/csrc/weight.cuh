@@ -1,0 +1,86 @@
+// weight.cuh -- the (cell, sample) kernel weight of Eq. 1 and its support test.
+//
+// PAPER.md:219-221 (Algorithm 1): "if d(target_cell[], raw_data[i]) <= R: compute weight
+// sum, compute weighted value"; w = exp(-d^2 / 2 sigma^2) (readings R1-R5).
+//
+// Hot path (fp32): the haversine
+//     h = sin^2(dlat/2) + cos(lat_c) cos(lat_s) sin^2(dlon/2),   d^2 = 4 asin^2(sqrt h)
+// evaluated by series on exact small offsets: dlat/dlon are (integer bin-to-cell offset +
+// the sample's fp32 offset from its bin centre) x cdelt, so no large absolute angles are
+// ever rounded to fp32.  Truncation of the series is < 3e-7 relative for R <= 1 deg
+// (plan-enforced).  The support test is decided in fp32 outside a +-1e-5 relative guard
+// band around R^2 and re-decided inside it by an fp64 haversine on the original fp64
+// coordinates, written out without FMA contraction, so the neighbour set is the fp64 one.
+#pragma once
+
+#include "common.cuh"
+
+namespace hg {
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ double wrap180_d(double x) {
+    double y = fmod(x, 360.0);
+    if (y > 180.0) y = __dadd_rn(y, -360.0);
+    if (y <= -180.0) y = __dadd_rn(y, 360.0);
+    return y;
+}
+
+// fp64 support test d <= R for cell (i, j) and a sample at (lon_s, lat_s) degrees.
+static __device__ __noinline__ bool support_fp64(const Geom& g, int i, int j, double lon_s,
+                                          double lat_s) {
+    double lon_c = __dadd_rn(g.crval_lon,
+                             __dmul_rn(__dadd_rn(__dadd_rn((double)i, 1.0), -g.crpix_x),
+                                       g.cdelt_lon));
+    double lat_c = __dadd_rn(g.crval_lat,
+                             __dmul_rn(__dadd_rn(__dadd_rn((double)j, 1.0), -g.crpix_y),
+                                       g.cdelt_lat));
+    double dlon = __dmul_rn(wrap180_d(__dadd_rn(lon_s, -lon_c)), kDeg2Rad);
+    double dlat = __dmul_rn(__dadd_rn(lat_s, -lat_c), kDeg2Rad);
+    double s1 = sin(__dmul_rn(0.5, dlat));
+    double s2 = sin(__dmul_rn(0.5, dlon));
+    double cc = __dmul_rn(cos(__dmul_rn(lat_c, kDeg2Rad)), cos(__dmul_rn(lat_s, kDeg2Rad)));
+    double h = __dadd_rn(__dmul_rn(s1, s1), __dmul_rn(cc, __dmul_rn(s2, s2)));
+    double r = sqrt(h);
+    if (r > 1.0) r = 1.0;
+    double d = __dmul_rn(2.0, asin(r));
+    return d <= g.R_rad;
+}
+
+// d^2 (rad^2) from offsets in cells; cc = cos(lat_c) * cos(lat_s).
+__device__ __forceinline__ float pair_d2(const Geom& g, float dx_cells, float dy_cells,
+                                         float cc) {
+    float a = dy_cells * (0.5f * g.dlat_rad);
+    float b = dx_cells * (0.5f * g.dlon_rad);
+    float a2 = a * a, b2 = b * b;
+    float sa = a2 * (1.0f - a2 * (1.0f / 3.0f));   // sin^2(dlat/2)
+    float sb = b2 * (1.0f - b2 * (1.0f / 3.0f));   // sin^2(dlon/2)
+    float h = sa + cc * sb;
+    return 4.0f * h * (1.0f + h * ((1.0f / 3.0f) + h * (8.0f / 45.0f)));  // 4 asin^2(sqrt h)
+}
+
+// Full weight: returns 0 outside the support.  (i, j) cell; geo = sample's plan data;
+// br = the sample's bin row; p = its plan position (for the fp64 recheck).
+__device__ __forceinline__ float pair_weight(const Geom& g, const PlanDev& pd, int i, int j,
+                                             float cos_c, int br, float4 geo, int p) {
+    int bc = __float_as_int(geo.w);
+    float dx = (float)(bc - g.mlon - i) + geo.x;
+    float dy = (float)(br - g.mlat - j) + geo.y;
+    float d2 = pair_d2(g, dx, dy, cos_c * geo.z);
+    bool in;
+    if (d2 <= g.R2_lo) {
+        in = true;
+    } else if (d2 > g.R2_hi) {
+        in = false;
+    } else {
+        double2 ll = pd.ll[p];
+        in = support_fp64(g, i, j, ll.x, ll.y);
+    }
+    return in ? ex2_approx(d2 * g.neg_k2) : 0.0f;
+}
+
+}  // namespace hg

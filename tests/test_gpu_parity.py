@@ -1,0 +1,262 @@
+"""GPU parity: the CUDA path through the C-ABI vs the fp64 oracle, element by element.
+
+Sizes are chosen so the oracle finishes in seconds while the GPU path still spans many
+CTA tiles, several channel blocks and ragged tails (map sizes not multiples of 8,
+channel counts not multiples of 128).  Full BASELINE sizes are covered by sampled
+checks in test_gpu_fullsize.py.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2207_04584_b200 import Plan, _binding as b
+from parity_util import compare, make_inputs, oracle_grid, plan_layout_values, small_workload
+
+pytestmark = pytest.mark.gpu
+
+
+# ------------------------------------------------------------------ plan layer
+def test_radix_sort_spec_example():
+    """pixel_idx [7,2,7,0,2] -> perm [3,1,4,0,2] (stable)."""
+    assert b.hegrid_sort_u32(np.array([7, 2, 7, 0, 2], np.uint32)).tolist() == [3, 1, 4, 0, 2]
+
+
+@pytest.mark.parametrize("n,hi", [(1, 5), (2, 1), (4095, 3), (4096, 1 << 17), (4097, 7),
+                                  (1_000_003, 1 << 17), (300_000, 1 << 32 - 1)])
+def test_radix_sort_matches_numpy_stable(n, hi):
+    rng = np.random.default_rng(n)
+    keys = rng.integers(0, hi, n, dtype=np.uint64).astype(np.uint32)
+    got = b.hegrid_sort_u32(keys)
+    ref = np.argsort(keys, kind="stable")
+    np.testing.assert_array_equal(got, ref)
+
+
+def test_radix_sort_degenerate():
+    assert b.hegrid_sort_u32(np.zeros(0, np.uint32)).shape == (0,)
+    keys = np.full(10_000, 42, np.uint32)
+    np.testing.assert_array_equal(b.hegrid_sort_u32(keys), np.arange(10_000))
+    keys = np.arange(10_000, dtype=np.uint32)[::-1].copy()
+    np.testing.assert_array_equal(b.hegrid_sort_u32(keys), np.arange(10_000)[::-1])
+
+
+def _cfg1():
+    w = synth.CONFIGS["cfg1"]
+    lon, lat, vals = make_inputs(w)
+    return w, lon.numpy(), lat.numpy(), vals.numpy()
+
+
+def test_neighbour_sets_exact_cfg1():
+    """Algorithm 1's set {n : d <= R}, computed through the plan's candidate ranges and
+    the fp32 + guard-band predicate, equals the fp64 oracle's set exactly (so the
+    candidate lookup misses nothing)."""
+    w, lon, lat, _ = _cfg1()
+    with Plan(lon, lat, w.map, w.fwhm_deg) as p:
+        off, idx = p.neighbours()
+        info = p.info()
+    ooff, oidx = oracle.neighbours(lon, lat, w.map, w.fwhm_deg)
+    np.testing.assert_array_equal(off, ooff)
+    np.testing.assert_array_equal(idx, oidx)
+    assert info["n_pairs"] == ooff[-1]
+    assert info["n_candidate_pairs"] >= info["n_pairs"]
+    assert info["n_used"] <= w.n
+
+
+def test_plan_permutation_is_stable_bin_order_cfg2_small():
+    w = small_workload("cfg2", n=200 * 150, tracks=200, per_track=150)
+    lon, lat = synth.coords(w)
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg) as p:
+        perm = p.permutation()
+        info = p.info()
+    assert len(set(perm.tolist())) == perm.shape[0] == info["n_used"]
+    # recompute each used sample's bin independently (nearest cell in the map frame)
+    m = w.map
+    x = (lon.numpy() - m["crval_lon"]) / m["cdelt_lon"] + m["crpix_x"] - 1
+    y = (lat.numpy() - m["crval_lat"]) / m["cdelt_lat"] + m["crpix_y"] - 1
+    key = (np.floor(y + 0.5) + info["mlat"]) * info["ncol"] + np.floor(x + 0.5) + info["mlon"]
+    k = key[perm]
+    assert np.all(np.diff(k) >= 0), "plan order is not bin order"
+    same = np.diff(k) == 0
+    assert np.all(np.diff(perm)[same] > 0), "ties not in original order (unstable)"
+
+
+# ------------------------------------------------------------------ Eq. 1 parity
+def test_grid_cfg1_full_parity():
+    """BASELINE configs[0] in full: 5000 samples, 64x64, 1 channel."""
+    w, lon, lat, vals = _cfg1()
+    with Plan(lon, lat, w.map, w.fwhm_deg) as p:
+        out, W = p.grid(vals)
+    o, Wo, _ = oracle_grid(w, lon, lat, vals)
+    st = compare(out.reshape(1, -1), W.reshape(-1), o, Wo)
+    assert st["covered"] == w.cells
+
+
+def test_grid_drift_scan_many_channels_ragged():
+    """cfg2-shaped drift scan at oracle-friendly size: 70x61 map (ragged tiles), 133
+    channels (two 128-channel blocks, ragged tail)."""
+    w = small_workload("cfg2", n=220 * 180, tracks=220, per_track=180, nx=70, ny=61,
+                       field_lon=1.2, field_lat=1.1, channels=133)
+    lon, lat, vals = make_inputs(w)
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg) as p:
+        out, W = p.grid(vals.numpy())
+    o, Wo, _ = oracle_grid(w, lon, lat, vals)
+    compare(out.reshape(133, -1), W.reshape(-1), o, Wo)
+
+
+def test_grid_high_density_cfg3_shape():
+    """cfg3's density (1e6 samples/deg^2) and kernel (FWHM 6.925', ~84k neighbours per
+    cell) on a 0.4 deg field, 24x24 map, 7 channels."""
+    w = small_workload("cfg3", n=160_000, field_lon=0.4, field_lat=0.4, nx=24, ny=24,
+                       channels=7)
+    lon, lat, vals = make_inputs(w)
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg) as p:
+        out, W = p.grid(vals.numpy())
+        info = p.info()
+    assert info["nbr_max"] > 20_000
+    o, Wo, _ = oracle_grid(w, lon, lat, vals)
+    compare(out.reshape(7, -1), W.reshape(-1), o, Wo)
+
+
+def test_device_paths_bit_identical_and_deterministic():
+    """Host path, device USER_CN path and device PLAN_NC path give bit-identical maps;
+    repeated runs are bit-identical (no atomics, fixed summation order)."""
+    w = small_workload("cfg2", n=120 * 100, tracks=120, per_track=100, nx=40, ny=37,
+                       field_lon=0.7, field_lat=0.6, channels=300)
+    lon, lat, vals = make_inputs(w)
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, n_streams=3, channel_block=64) as p:
+        out_h, W_h = p.grid(vals.numpy())
+        out_h2, _ = p.grid(vals.numpy())
+        d = vals.cuda()
+        out_d, W_d = p.grid(d)
+        perm = p.permutation()
+        vp = plan_layout_values(w, lon, lat, perm, list(range(300)))
+        out_p = torch.empty_like(out_d)
+        W_p = torch.empty_like(W_d)
+        p.grid_plan_layout(vp, 300, out_p, W_p)
+        torch.cuda.synchronize()
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, n_streams=1, channel_block=300) as p2:
+        out_h3, _ = p2.grid(vals.numpy())
+    np.testing.assert_array_equal(out_h, out_h2)
+    np.testing.assert_array_equal(out_h, out_d.cpu().numpy())
+    np.testing.assert_array_equal(out_h, out_p.cpu().numpy())
+    np.testing.assert_array_equal(out_h, out_h3)
+    np.testing.assert_array_equal(W_h, W_d.cpu().numpy())
+    np.testing.assert_array_equal(W_h, W_p.cpu().numpy())
+
+
+def test_permute_kernel_exact():
+    w = small_workload("cfg2", n=90 * 70, tracks=90, per_track=70, nx=30, ny=30,
+                       field_lon=0.6, field_lat=0.6, channels=37)
+    lon, lat, vals = make_inputs(w)
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg) as p:
+        perm = torch.as_tensor(p.permutation())
+        d = vals.cuda()
+        vp = torch.full((perm.shape[0], 40), -1.0, device="cuda")
+        p.permute(d, vp)
+        torch.cuda.synchronize()
+    ref = vals[:, perm].t()
+    assert torch.equal(vp[:, :37].cpu(), ref)
+
+
+# ------------------------------------------------------------------ edge cases
+def _one_channel(lon, lat, v, m, fwhm):
+    with Plan(np.asarray(lon, np.float64), np.asarray(lat, np.float64), m, fwhm) as p:
+        out, W = p.grid(np.asarray(v, np.float32)[None])
+    o, Wo, _ = oracle.grid(np.asarray(lon), np.asarray(lat), np.asarray(v, np.float32)[None],
+                           m, fwhm)
+    return out.reshape(1, -1), W.reshape(-1), o, Wo
+
+
+def mk_map(nx, ny, lon0, lat0, dl, dlat=None):
+    return dict(nx=nx, ny=ny, crval_lon=lon0, crval_lat=lat0, crpix_x=(nx + 1) / 2,
+                crpix_y=(ny + 1) / 2, cdelt_lon=dl, cdelt_lat=dl if dlat is None else dlat)
+
+
+def test_empty_input_all_blank():
+    m = mk_map(9, 7, 30, 41, 1 / 60)
+    with Plan(np.zeros(0), np.zeros(0), m, 0.05) as p:
+        out, W = p.grid(np.zeros((3, 0), np.float32))
+    assert np.all(np.isnan(out)) and np.all(W == 0)
+
+
+def test_zero_channels_writes_weight_map():
+    rng = np.random.default_rng(0)
+    lon = 30 + rng.uniform(-0.1, 0.1, 500)
+    lat = 41 + rng.uniform(-0.1, 0.1, 500)
+    m = mk_map(11, 13, 30, 41, 1 / 60)
+    with Plan(lon, lat, m, 0.05) as p:
+        out, W = p.grid(np.zeros((0, 500), np.float32))
+    _, Wo, _ = oracle.grid(lon, lat, None, m, 0.05)
+    np.testing.assert_allclose(W.reshape(-1), Wo, rtol=1e-5)
+
+
+def test_sample_at_cell_centre_weight_one_and_outside_samples_dropped():
+    m = mk_map(16, 16, 30, 41, 1 / 60)
+    lon_c, lat_c = oracle.cell_centre(m, 5, 9)
+    lon = np.array([lon_c, 31.5, 28.0, lon_c])
+    lat = np.array([lat_c, 41.0, 45.0, lat_c + 0.9 / 60])
+    out, W, o, Wo = _one_channel(lon, lat, [5.0, 1.0, 2.0, 7.0], m, 0.05)
+    compare(out, W, o, Wo)
+    with Plan(lon, lat, m, 0.05) as p:
+        assert p.info()["n_used"] == 2
+
+
+def test_negative_cdelt_and_lon_zero_straddle():
+    rng = np.random.default_rng(4)
+    lon = (rng.uniform(-0.25, 0.25, 6000) + 360.0) % 360.0
+    lat = rng.uniform(-0.2, 0.2, 6000)
+    m = mk_map(29, 23, 0.0, 0.0, -1 / 60, 1 / 60)
+    v = 10 + rng.normal(0, 1, 6000)
+    compare(*_one_channel(lon, lat, v, m, 0.05))
+
+
+def test_support_edge_guard_band():
+    """Samples at d = R(1 +- 1e-7) from a cell on the equator: inside the fp32 guard band,
+    decided by the fp64 recheck exactly like the oracle."""
+    m = mk_map(1, 1, 10.0, 0.0, 1 / 60)
+    R = 3 * 0.05 / (2 * math.sqrt(2 * math.log(2)))
+    lon = np.array([10 + R * (1 - 1e-7), 10 - R * (1 + 1e-7), 10.0, 10.0])
+    lat = np.array([0.0, 0.0, R * (1 - 1e-9), -R * (1 + 1e-9)])
+    with Plan(lon, lat, m, 0.05) as p:
+        off, idx = p.neighbours()
+    ooff, oidx = oracle.neighbours(lon, lat, m, 0.05)
+    assert idx.tolist() == oidx.tolist() == [0, 2]
+
+
+def test_domain_and_unsupported_errors():
+    m = mk_map(8, 8, 30, 41, 1 / 60)
+    with pytest.raises(b.HegridError) as e:
+        Plan(np.array([30.0, np.nan]), np.array([41.0, 41.0]), m, 0.05)
+    assert e.value.code == 2
+    with pytest.raises(b.HegridError) as e:
+        Plan(np.array([30.0]), np.array([91.0]), m, 0.05)
+    assert e.value.code == 2
+    with pytest.raises(b.HegridError) as e:
+        Plan(np.array([30.0]), np.array([41.0]), m, 1.0)        # R = 1.27 deg > 1 deg
+    assert e.value.code == 5
+    with pytest.raises(b.HegridError) as e:
+        Plan(np.array([30.0]), np.array([88.9]), mk_map(8, 8, 30, 88.9, 1 / 60), 0.05)
+    assert e.value.code == 5
+
+
+def test_device_coordinate_plan_matches_host_plan():
+    w = small_workload("cfg2", n=80 * 60, tracks=80, per_track=60, nx=24, ny=20,
+                       field_lon=0.4, field_lat=0.35, channels=5)
+    lon, lat, vals = make_inputs(w)
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg) as p1, \
+            Plan(lon.cuda(), lat.cuda(), w.map, w.fwhm_deg) as p2:
+        np.testing.assert_array_equal(p1.permutation(), p2.permutation())
+        a, _ = p1.grid(vals.numpy())
+        bb, _ = p2.grid(vals.numpy())
+    np.testing.assert_array_equal(a, bb)
+
+
+def test_launches_are_counted():
+    before = b.hegrid_launch_count()
+    w, lon, lat, vals = _cfg1()
+    with Plan(lon, lat, w.map, w.fwhm_deg) as p:
+        p.grid(vals)
+    assert b.hegrid_launch_count() > before
