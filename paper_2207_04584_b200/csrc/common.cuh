@@ -65,6 +65,7 @@ struct hegrid_plan_s {
     int* d_mrow = nullptr;
     float* d_cos_row = nullptr;
     double t_plan_ms = 0;
+    int64_t max_cand = 0;           // max candidate-range length over cells
     bool stats_valid = false;
     hegrid_plan_stats stats{};
     // profiling

@@ -30,7 +30,7 @@ __device__ __forceinline__ float4 ldg_nc(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
-template <int QC>
+template <int QC, bool SPLIT>
 __global__ void __launch_bounds__(SIMT_THREADS) k_accum_simt(const __grid_constant__ Geom g, PlanDev pd,
                                                              const float* __restrict__ V,
                                                              int64_t ldv, int C,
@@ -75,6 +75,15 @@ __global__ void __launch_bounds__(SIMT_THREADS) k_accum_simt(const __grid_consta
         for (int c = 0; c < BW; ++c) cok[c] = bi0 + c < g.nx;
 
         for (int br = bj0; br <= j_hi + 2 * g.mlat; ++br) {
+            // SPLIT: per-bin-row partial sums (two-level summation keeps the fp32 rounding
+            // of ~1e5-term sums well inside 1e-5)
+            float part[SPLIT ? 8 : 1][SPLIT ? QC : 1];
+            if constexpr (SPLIT) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+#pragma unroll
+                    for (int q = 0; q < QC; ++q) part[k][q] = 0.0f;
+            }
             const int m = pd.mrow[br];
             const int64_t rowb = (int64_t)br * g.ncol;
             const uint32_t s0 = pd.bin_start[rowb + bi0 + g.mlon - m];
@@ -123,9 +132,20 @@ __global__ void __launch_bounds__(SIMT_THREADS) k_accum_simt(const __grid_consta
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
 #pragma unroll
-                        for (int q = 0; q < QC; ++q) acc[k][q] = fmaf(ww[k], v[q], acc[k][q]);
+                        for (int q = 0; q < QC; ++q) {
+                            if constexpr (SPLIT)
+                                part[k][q] = fmaf(ww[k], v[q], part[k][q]);
+                            else
+                                acc[k][q] = fmaf(ww[k], v[q], acc[k][q]);
+                        }
                 }
                 __syncwarp();
+            }
+            if constexpr (SPLIT) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+#pragma unroll
+                    for (int q = 0; q < QC; ++q) acc[k][q] += part[k][q];
             }
         }
     }
@@ -164,16 +184,16 @@ __global__ void __launch_bounds__(SIMT_THREADS) k_accum_simt(const __grid_consta
     }
 }
 
-template <int QC>
+template <int QC, bool SPLIT>
 static hegrid_status launch_qc(const hegrid_plan_s* p, const float* d_v, int64_t ldv, int C,
                                float* d_out, float* d_w, cudaStream_t st) {
     const Geom& g = p->g;
     int tiles = ((g.nx + TW - 1) / TW) * ((g.ny + TH - 1) / TH);
     dim3 grid(tiles, (C + 32 * QC - 1) / (32 * QC));
     size_t smem = sizeof(float) * (32 * QC) * (TW * TH + 1);
-    HG_TRY(cudaFuncSetAttribute(k_accum_simt<QC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HG_TRY(cudaFuncSetAttribute(k_accum_simt<QC, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
-    k_accum_simt<QC><<<grid, SIMT_THREADS, smem, st>>>(g, p->dev(), d_v, ldv, C, d_out, d_w);
+    k_accum_simt<QC, SPLIT><<<grid, SIMT_THREADS, smem, st>>>(g, p->dev(), d_v, ldv, C, d_out, d_w);
     count_launch();
     return cuda_status(cudaGetLastError());
 }
@@ -184,8 +204,10 @@ hegrid_status launch_accumulate_simt(const hegrid_plan_s* p, const float* d_v, i
     if (n_channels <= 0) return HEGRID_OK;
     if (n_channels > (1LL << 30)) return HEGRID_EINVAL;
     int C = (int)n_channels;
-    if (C >= 512) return launch_qc<8>(p, d_v, ldv, C, d_out, d_weight, st);
-    return launch_qc<4>(p, d_v, ldv, C, d_out, d_weight, st);
+    // dense regime (long per-cell sums): two-level summation, 4 channels per lane
+    if (p->max_cand > 2048) return launch_qc<4, true>(p, d_v, ldv, C, d_out, d_weight, st);
+    if (C >= 512) return launch_qc<8, false>(p, d_v, ldv, C, d_out, d_weight, st);
+    return launch_qc<4, false>(p, d_v, ldv, C, d_out, d_weight, st);
 }
 
 }  // namespace hg

@@ -319,7 +319,19 @@ hegrid_status build_plan(hegrid_plan_s* p, const double* d_lon, const double* d_
                                                             p->d_bin_start);
     count_launch();
     HG_TRY(cudaGetLastError());
+    unsigned long long* d_mx = nullptr;
+    HG_TRY(cudaMallocAsync(&d_mx, sizeof(unsigned long long), st));
+    HG_TRY(cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long), st));
+    {
+        int64_t cells = (int64_t)g.nx * g.ny;
+        k_max_cand<<<(int)((cells + 255) / 256), 256, 0, st>>>(g, p->dev(), d_mx);
+        count_launch();
+    }
+    HG_TRY(cudaGetLastError());
     HG_TRY(cudaEventRecord(e1, st));
+    unsigned long long mx = 0;
+    HG_TRY(cudaMemcpyAsync(&mx, d_mx, sizeof(mx), cudaMemcpyDeviceToHost, st));
+    HG_TRY(cudaFreeAsync(d_mx, st));
     int bad = 0;
     uint32_t used = 0;
     HG_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -334,10 +346,26 @@ hegrid_status build_plan(hegrid_plan_s* p, const double* d_lon, const double* d_
     p->t_plan_ms = ms;
     if (bad) return HEGRID_EDOMAIN;
     p->n_used = used;
+    p->max_cand = (int64_t)mx;
     return HEGRID_OK;
 }
 
 // ------------------------------------------------------------------ statistics / neighbours
+// One thread per cell: candidate-range length only -> max over cells (kernel selection).
+__global__ void k_max_cand(const __grid_constant__ Geom g, PlanDev pd,
+                           unsigned long long* __restrict__ mx) {
+    int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (cell >= (int64_t)g.nx * g.ny) return;
+    int i = (int)(cell % g.nx), j = (int)(cell / g.nx);
+    unsigned long long nc = 0;
+    for (int br = j; br <= j + 2 * g.mlat; ++br) {
+        int m = pd.mrow[br];
+        int64_t rowb = (int64_t)br * g.ncol;
+        nc += pd.bin_start[rowb + i + g.mlon + m + 1] - pd.bin_start[rowb + i + g.mlon - m];
+    }
+    atomicMax(mx, nc);
+}
+
 // One thread per cell: candidate-range length and neighbour count.
 __global__ void k_cell_counts(const __grid_constant__ Geom g, PlanDev pd, int64_t c0, int64_t c1,
                               int64_t* __restrict__ cand, int64_t* __restrict__ nbr) {
