@@ -30,8 +30,20 @@ __device__ __forceinline__ float4 ldg_nc(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
+template <int QC>
+__device__ __forceinline__ void load_row(const float* p, bool ok, float* v) {
+#pragma unroll
+    for (int q4 = 0; q4 < QC; q4 += 4) {
+        float4 x = ok ? ldg_nc(p + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[q4] = x.x;
+        v[q4 + 1] = x.y;
+        v[q4 + 2] = x.z;
+        v[q4 + 3] = x.w;
+    }
+}
+
 template <int QC, bool SPLIT>
-__global__ void __launch_bounds__(SIMT_THREADS) k_accum_simt(const __grid_constant__ Geom g, PlanDev pd,
+__global__ void __launch_bounds__(SIMT_THREADS, (QC == 4 && !SPLIT) ? 2 : 1) k_accum_simt(const __grid_constant__ Geom g, PlanDev pd,
                                                              const float* __restrict__ V,
                                                              int64_t ldv, int C,
                                                              float* __restrict__ out,
@@ -114,18 +126,25 @@ __global__ void __launch_bounds__(SIMT_THREADS) k_accum_simt(const __grid_consta
                 wbuf[warp][lane][1] = make_float4(w[4], w[5], w[6], w[7]);
                 uint32_t mask = __ballot_sync(0xffffffffu, nz);
                 __syncwarp();
-                while (mask) {
-                    const int t = __ffs(mask) - 1;
+                // software pipeline: the value row of the next active sample is in flight
+                // while the rank-1 update of the current one issues
+                float vn[QC];
+                int tn = -1;
+                if (mask) {
+                    tn = __ffs(mask) - 1;
                     mask &= mask - 1;
-                    const float* vp = V + (int64_t)(base + t) * ldv + c_lane;
+                    load_row<QC>(V + (int64_t)(base + tn) * ldv + c_lane, ch_ok, vn);
+                }
+                while (tn >= 0) {
+                    const int t = tn;
                     float v[QC];
 #pragma unroll
-                    for (int q4 = 0; q4 < QC; q4 += 4) {
-                        float4 x = ch_ok ? ldg_nc(vp + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
-                        v[q4] = x.x;
-                        v[q4 + 1] = x.y;
-                        v[q4 + 2] = x.z;
-                        v[q4 + 3] = x.w;
+                    for (int q = 0; q < QC; ++q) v[q] = vn[q];
+                    tn = -1;
+                    if (mask) {
+                        tn = __ffs(mask) - 1;
+                        mask &= mask - 1;
+                        load_row<QC>(V + (int64_t)(base + tn) * ldv + c_lane, ch_ok, vn);
                     }
                     const float4 wa = wbuf[warp][t][0], wb = wbuf[warp][t][1];
                     const float ww[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
@@ -206,7 +225,6 @@ hegrid_status launch_accumulate_simt(const hegrid_plan_s* p, const float* d_v, i
     int C = (int)n_channels;
     // dense regime (long per-cell sums): two-level summation, 4 channels per lane
     if (p->max_cand > 2048) return launch_qc<4, true>(p, d_v, ldv, C, d_out, d_weight, st);
-    if (C >= 512) return launch_qc<8, false>(p, d_v, ldv, C, d_out, d_weight, st);
     return launch_qc<4, false>(p, d_v, ldv, C, d_out, d_weight, st);
 }
 

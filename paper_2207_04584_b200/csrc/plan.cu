@@ -210,6 +210,21 @@ __global__ void k_gather(const __grid_constant__ Geom g, const double* __restric
     ll[p] = make_double2(lo, la);
 }
 
+// One thread per cell: candidate-range length only -> max over cells (kernel selection).
+__global__ void k_max_cand(const __grid_constant__ Geom g, PlanDev pd,
+                           unsigned long long* __restrict__ mx) {
+    int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (cell >= (int64_t)g.nx * g.ny) return;
+    int i = (int)(cell % g.nx), j = (int)(cell / g.nx);
+    unsigned long long nc = 0;
+    for (int br = j; br <= j + 2 * g.mlat; ++br) {
+        int m = pd.mrow[br];
+        int64_t rowb = (int64_t)br * g.ncol;
+        nc += pd.bin_start[rowb + i + g.mlon + m + 1] - pd.bin_start[rowb + i + g.mlon - m];
+    }
+    atomicMax(mx, nc);
+}
+
 // ------------------------------------------------------------------ host: geometry
 static hegrid_status make_geom(hegrid_plan_s* p, std::vector<int>& mrow,
                                std::vector<float>& cos_row) {
@@ -351,21 +366,6 @@ hegrid_status build_plan(hegrid_plan_s* p, const double* d_lon, const double* d_
 }
 
 // ------------------------------------------------------------------ statistics / neighbours
-// One thread per cell: candidate-range length only -> max over cells (kernel selection).
-__global__ void k_max_cand(const __grid_constant__ Geom g, PlanDev pd,
-                           unsigned long long* __restrict__ mx) {
-    int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (cell >= (int64_t)g.nx * g.ny) return;
-    int i = (int)(cell % g.nx), j = (int)(cell / g.nx);
-    unsigned long long nc = 0;
-    for (int br = j; br <= j + 2 * g.mlat; ++br) {
-        int m = pd.mrow[br];
-        int64_t rowb = (int64_t)br * g.ncol;
-        nc += pd.bin_start[rowb + i + g.mlon + m + 1] - pd.bin_start[rowb + i + g.mlon - m];
-    }
-    atomicMax(mx, nc);
-}
-
 // One thread per cell: candidate-range length and neighbour count.
 __global__ void k_cell_counts(const __grid_constant__ Geom g, PlanDev pd, int64_t c0, int64_t c1,
                               int64_t* __restrict__ cand, int64_t* __restrict__ nbr) {
