@@ -217,6 +217,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--engine", default="tc", choices=["simt", "tc", "auto"])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -238,7 +239,8 @@ def main():
 
     # ---------------------------------------------------------------- plan (once)
     stream = torch.cuda.current_stream(dev)
-    plan = Plan(lon, lat, w.map, w.fwhm_deg, w.support, device=local, stream=stream)
+    plan = Plan(lon, lat, w.map, w.fwhm_deg, w.support, device=local, stream=stream,
+                engine=args.engine)
     info = plan.info()
     perm = torch.as_tensor(plan.permutation(), device=dev)
     vp = plan_layout_values(w, lon, lat, perm, channel_ids, dev)
@@ -325,7 +327,8 @@ def main():
         lat_h = lat.cpu().numpy()
 
         def e2e_step():
-            with Plan(lon_h, lat_h, w.map, w.fwhm_deg, w.support, device=local) as p:
+            with Plan(lon_h, lat_h, w.map, w.fwhm_deg, w.support, device=local,
+                      engine=args.engine) as p:
                 p.grid(host_vals, host_out, host_w)
             return float(host_w[w.ny // 2, w.nx // 2])   # read of the result
         e2e_step()

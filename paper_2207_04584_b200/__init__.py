@@ -9,7 +9,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _binding as abi
-from ._binding import (HEGRID_LAYOUT_PLAN_NC, HEGRID_LAYOUT_USER_CN, HegridError,  # noqa: F401
+from ._binding import (HEGRID_ENGINE_TC, HEGRID_LAYOUT_PLAN_NC, HEGRID_LAYOUT_USER_CN, HegridError,  # noqa: F401
                        hegrid_abi_version, hegrid_grid, hegrid_grid_device,
                        hegrid_launch_count, hegrid_neighbours, hegrid_permute_device,
                        hegrid_plan_create, hegrid_plan_create_device, hegrid_plan_destroy,
@@ -38,12 +38,14 @@ class Plan:
     cdelt_lon, cdelt_lat.
     """
 
+    ENGINES = {"auto": 0, "simt": 1, "tc": 2}
+
     def __init__(self, lon, lat, map, fwhm_deg, support_sigma=3.0, device=0, n_streams=0,
-                 channel_block=0, stream=None):
+                 channel_block=0, stream=None, engine="auto"):
         self.map = dict(map) if isinstance(map, dict) else map
         self.nx, self.ny = int(self.map["nx"]), int(self.map["ny"])
         self.device = device
-        opts = make_opts(device, n_streams, channel_block)
+        opts = make_opts(device, n_streams, channel_block, self.ENGINES[engine])
         if hasattr(lon, "is_cuda") and lon.is_cuda:
             import torch
             lon = lon.to(torch.float64).contiguous()

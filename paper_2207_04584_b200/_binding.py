@@ -21,6 +21,7 @@ HEGRID_LAYOUT_USER_CN = 0
 HEGRID_LAYOUT_PLAN_NC = 1
 HEGRID_ENGINE_AUTO = 0
 HEGRID_ENGINE_SIMT = 1
+HEGRID_ENGINE_TC = 2
 
 
 class HegridError(RuntimeError):

@@ -94,6 +94,14 @@ static hegrid_status create_common(const double* d_lon, const double* d_lat, int
     return HEGRID_OK;
 }
 
+hegrid_status launch_accumulate(const hegrid_plan_s* p, const float* d_v, int64_t ldv,
+                                int64_t n_channels, float* d_out, float* d_weight,
+                                cudaStream_t st) {
+    if (p->opts.engine == HEGRID_ENGINE_TC)
+        return launch_accumulate_tc(p, d_v, ldv, n_channels, d_out, d_weight, st);
+    return launch_accumulate_simt(p, d_v, ldv, n_channels, d_out, d_weight, st);
+}
+
 }  // namespace hg
 
 using namespace hg;
@@ -216,12 +224,12 @@ hegrid_status hegrid_permute_device(hegrid_plan_t p, const float* d_user, int64_
 
 static hegrid_status accumulate_profiled(hegrid_plan_s* p, const float* d_v, int64_t ldv,
                                          int64_t C, float* d_out, float* d_w, cudaStream_t st) {
-    if (!p->profile) return launch_accumulate_simt(p, d_v, ldv, C, d_out, d_w, st);
+    if (!p->profile) return launch_accumulate(p, d_v, ldv, C, d_out, d_w, st);
     cudaEvent_t a, b;
     HG_TRY(cudaEventCreate(&a));
     HG_TRY(cudaEventCreate(&b));
     HG_TRY(cudaEventRecord(a, st));
-    hegrid_status s = launch_accumulate_simt(p, d_v, ldv, C, d_out, d_w, st);
+    hegrid_status s = launch_accumulate(p, d_v, ldv, C, d_out, d_w, st);
     HG_TRY(cudaEventRecord(b, st));
     p->prof_events.push_back(a);
     p->prof_events.push_back(b);
@@ -236,7 +244,7 @@ static hegrid_status weights_only(hegrid_plan_s* p, float* d_w, cudaStream_t st)
     HG_TRY(cudaMallocAsync(&z, nz * sizeof(float), st));
     HG_TRY(cudaMallocAsync(&o, (size_t)p->g.nx * p->g.ny * sizeof(float), st));
     HG_TRY(cudaMemsetAsync(z, 0, nz * sizeof(float), st));
-    hegrid_status s = launch_accumulate_simt(p, z, 4, 1, o, d_w, st);
+    hegrid_status s = launch_accumulate(p, z, 4, 1, o, d_w, st);
     cudaFreeAsync(z, st);
     cudaFreeAsync(o, st);
     return s;
@@ -356,7 +364,7 @@ hegrid_status hegrid_grid(hegrid_plan_t p, const float* data, int64_t n_channels
                 break;
             if ((s = launch_permute(p, x.d_raw, cn, n, x.d_v, cb, x.st)) != HEGRID_OK) break;
         }
-        if ((s = launch_accumulate_simt(p, x.d_v, cb, cn, x.d_out, b == 0 ? d_w : nullptr,
+        if ((s = launch_accumulate(p, x.d_v, cb, cn, x.d_out, b == 0 ? d_w : nullptr,
                                         x.st)) != HEGRID_OK)
             break;
         float* dst = out_pinned ? out_map + c0 * cells : x.h_out;

@@ -95,6 +95,14 @@ hegrid_status plan_neighbours(hegrid_plan_s* p, int64_t c0, int64_t c1, int64_t*
 hegrid_status launch_accumulate_simt(const hegrid_plan_s* p, const float* d_v, int64_t ldv,
                                      int64_t n_channels, float* d_out, float* d_weight,
                                      cudaStream_t st);
+// grid_tc.cu
+hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int64_t ldv,
+                                   int64_t n_channels, float* d_out, float* d_weight,
+                                   cudaStream_t st);
+// engine dispatch (api.cu)
+hegrid_status launch_accumulate(const hegrid_plan_s* p, const float* d_v, int64_t ldv,
+                                int64_t n_channels, float* d_out, float* d_weight,
+                                cudaStream_t st);
 // permute.cu
 hegrid_status launch_permute(const hegrid_plan_s* p, const float* d_user, int64_t n_channels,
                              int64_t ld_user, float* d_plan, int64_t ld_plan, cudaStream_t st);

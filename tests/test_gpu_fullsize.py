@@ -26,13 +26,14 @@ def sample_channels(C, k=12):
     return np.array(ch, np.int64)
 
 
+@pytest.mark.parametrize("engine", ["simt", "tc"])
 @pytest.mark.parametrize("name,channels", [("cfg2", None), ("cfg3", None), ("cfg4", None),
                                            ("cfg5", 260)])
-def test_fullsize_sampled_parity(name, channels):
+def test_fullsize_sampled_parity(name, channels, engine):
     w = synth.CONFIGS[name]
     C = w.channels if channels is None else channels
     lon, lat = synth.coords(w, device="cuda")
-    with Plan(lon, lat, w.map, w.fwhm_deg) as p:
+    with Plan(lon, lat, w.map, w.fwhm_deg, engine=engine) as p:
         perm = torch.as_tensor(p.permutation(), device="cuda")
         vp = plan_layout_values(w, lon, lat, perm, list(range(C)))
         out = torch.empty((C, w.ny, w.nx), device="cuda")

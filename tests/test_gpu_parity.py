@@ -18,6 +18,8 @@ from parity_util import compare, make_inputs, oracle_grid, plan_layout_values, s
 
 pytestmark = pytest.mark.gpu
 
+ENGINES = ["simt", "tc"]
+
 
 # ------------------------------------------------------------------ plan layer
 def test_radix_sort_spec_example():
@@ -84,35 +86,38 @@ def test_plan_permutation_is_stable_bin_order_cfg2_small():
 
 
 # ------------------------------------------------------------------ Eq. 1 parity
-def test_grid_cfg1_full_parity():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_grid_cfg1_full_parity(engine):
     """BASELINE configs[0] in full: 5000 samples, 64x64, 1 channel."""
     w, lon, lat, vals = _cfg1()
-    with Plan(lon, lat, w.map, w.fwhm_deg) as p:
+    with Plan(lon, lat, w.map, w.fwhm_deg, engine=engine) as p:
         out, W = p.grid(vals)
     o, Wo, _ = oracle_grid(w, lon, lat, vals)
     st = compare(out.reshape(1, -1), W.reshape(-1), o, Wo)
     assert st["covered"] == w.cells
 
 
-def test_grid_drift_scan_many_channels_ragged():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_grid_drift_scan_many_channels_ragged(engine):
     """cfg2-shaped drift scan at oracle-friendly size: 70x61 map (ragged tiles), 133
     channels (two 128-channel blocks, ragged tail)."""
     w = small_workload("cfg2", n=220 * 180, tracks=220, per_track=180, nx=70, ny=61,
                        field_lon=1.2, field_lat=1.1, channels=133)
     lon, lat, vals = make_inputs(w)
-    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg) as p:
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, engine=engine) as p:
         out, W = p.grid(vals.numpy())
     o, Wo, _ = oracle_grid(w, lon, lat, vals)
     compare(out.reshape(133, -1), W.reshape(-1), o, Wo)
 
 
-def test_grid_high_density_cfg3_shape():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_grid_high_density_cfg3_shape(engine):
     """cfg3's density (1e6 samples/deg^2) and kernel (FWHM 6.925', ~84k neighbours per
     cell) on a 0.4 deg field, 24x24 map, 7 channels."""
     w = small_workload("cfg3", n=160_000, field_lon=0.4, field_lat=0.4, nx=24, ny=24,
                        channels=7)
     lon, lat, vals = make_inputs(w)
-    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg) as p:
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, engine=engine) as p:
         out, W = p.grid(vals.numpy())
         info = p.info()
     assert info["nbr_max"] > 20_000
@@ -120,13 +125,15 @@ def test_grid_high_density_cfg3_shape():
     compare(out.reshape(7, -1), W.reshape(-1), o, Wo)
 
 
-def test_device_paths_bit_identical_and_deterministic():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_device_paths_bit_identical_and_deterministic(engine):
     """Host path, device USER_CN path and device PLAN_NC path give bit-identical maps;
     repeated runs are bit-identical (no atomics, fixed summation order)."""
     w = small_workload("cfg2", n=120 * 100, tracks=120, per_track=100, nx=40, ny=37,
                        field_lon=0.7, field_lat=0.6, channels=300)
     lon, lat, vals = make_inputs(w)
-    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, n_streams=3, channel_block=64) as p:
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, n_streams=3, channel_block=64,
+              engine=engine) as p:
         out_h, W_h = p.grid(vals.numpy())
         out_h2, _ = p.grid(vals.numpy())
         d = vals.cuda()
@@ -137,7 +144,8 @@ def test_device_paths_bit_identical_and_deterministic():
         W_p = torch.empty_like(W_d)
         p.grid_plan_layout(vp, 300, out_p, W_p)
         torch.cuda.synchronize()
-    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, n_streams=1, channel_block=300) as p2:
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, n_streams=1, channel_block=300,
+              engine=engine) as p2:
         out_h3, _ = p2.grid(vals.numpy())
     np.testing.assert_array_equal(out_h, out_h2)
     np.testing.assert_array_equal(out_h, out_d.cpu().numpy())
@@ -162,8 +170,9 @@ def test_permute_kernel_exact():
 
 
 # ------------------------------------------------------------------ edge cases
-def _one_channel(lon, lat, v, m, fwhm):
-    with Plan(np.asarray(lon, np.float64), np.asarray(lat, np.float64), m, fwhm) as p:
+def _one_channel(lon, lat, v, m, fwhm, engine="simt"):
+    with Plan(np.asarray(lon, np.float64), np.asarray(lat, np.float64), m, fwhm,
+              engine=engine) as p:
         out, W = p.grid(np.asarray(v, np.float32)[None])
     o, Wo, _ = oracle.grid(np.asarray(lon), np.asarray(lat), np.asarray(v, np.float32)[None],
                            m, fwhm)
@@ -175,42 +184,46 @@ def mk_map(nx, ny, lon0, lat0, dl, dlat=None):
                 crpix_y=(ny + 1) / 2, cdelt_lon=dl, cdelt_lat=dl if dlat is None else dlat)
 
 
-def test_empty_input_all_blank():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_empty_input_all_blank(engine):
     m = mk_map(9, 7, 30, 41, 1 / 60)
-    with Plan(np.zeros(0), np.zeros(0), m, 0.05) as p:
+    with Plan(np.zeros(0), np.zeros(0), m, 0.05, engine=engine) as p:
         out, W = p.grid(np.zeros((3, 0), np.float32))
     assert np.all(np.isnan(out)) and np.all(W == 0)
 
 
-def test_zero_channels_writes_weight_map():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_zero_channels_writes_weight_map(engine):
     rng = np.random.default_rng(0)
     lon = 30 + rng.uniform(-0.1, 0.1, 500)
     lat = 41 + rng.uniform(-0.1, 0.1, 500)
     m = mk_map(11, 13, 30, 41, 1 / 60)
-    with Plan(lon, lat, m, 0.05) as p:
+    with Plan(lon, lat, m, 0.05, engine=engine) as p:
         out, W = p.grid(np.zeros((0, 500), np.float32))
     _, Wo, _ = oracle.grid(lon, lat, None, m, 0.05)
     np.testing.assert_allclose(W.reshape(-1), Wo, rtol=1e-5)
 
 
-def test_sample_at_cell_centre_weight_one_and_outside_samples_dropped():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_sample_at_cell_centre_weight_one_and_outside_samples_dropped(engine):
     m = mk_map(16, 16, 30, 41, 1 / 60)
     lon_c, lat_c = oracle.cell_centre(m, 5, 9)
     lon = np.array([lon_c, 31.5, 28.0, lon_c])
     lat = np.array([lat_c, 41.0, 45.0, lat_c + 0.9 / 60])
-    out, W, o, Wo = _one_channel(lon, lat, [5.0, 1.0, 2.0, 7.0], m, 0.05)
+    out, W, o, Wo = _one_channel(lon, lat, [5.0, 1.0, 2.0, 7.0], m, 0.05, engine)
     compare(out, W, o, Wo)
     with Plan(lon, lat, m, 0.05) as p:
         assert p.info()["n_used"] == 2
 
 
-def test_negative_cdelt_and_lon_zero_straddle():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_negative_cdelt_and_lon_zero_straddle(engine):
     rng = np.random.default_rng(4)
     lon = (rng.uniform(-0.25, 0.25, 6000) + 360.0) % 360.0
     lat = rng.uniform(-0.2, 0.2, 6000)
     m = mk_map(29, 23, 0.0, 0.0, -1 / 60, 1 / 60)
     v = 10 + rng.normal(0, 1, 6000)
-    compare(*_one_channel(lon, lat, v, m, 0.05))
+    compare(*_one_channel(lon, lat, v, m, 0.05, engine))
 
 
 def test_support_edge_guard_band():

@@ -16,11 +16,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="cfg4")
 ap.add_argument("--channels", type=int, default=0)
 ap.add_argument("--launches", type=int, default=2)
+ap.add_argument("--engine", default="tc")
 a = ap.parse_args()
 w = synth.CONFIGS[a.workload]
 C = a.channels or w.channels
 lon, lat = synth.coords(w, device="cuda")
-p = Plan(lon, lat, w.map, w.fwhm_deg, w.support)
+p = Plan(lon, lat, w.map, w.fwhm_deg, w.support, engine=a.engine)
 perm = torch.as_tensor(p.permutation(), device="cuda")
 vp = plan_layout_values(w, lon, lat, perm, list(range(C)), "cuda")
 out = torch.empty((C, w.ny, w.nx), device="cuda")
