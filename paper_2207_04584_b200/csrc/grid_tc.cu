@@ -28,6 +28,8 @@
 //                     than ~10^3 MMA partials (tensor-core accumulation is not fp32-RN).
 // Epilogue: tcgen05.ld of each block's D, V = S / W (IEEE div), NaN where W = 0.
 // Deterministic: fixed chunk order, fixed work mapping, no atomics.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "tc_ptx.cuh"
 #include "weight.cuh"
@@ -127,7 +129,7 @@ struct ChunkWalk {
 template <bool PROMOTE>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const float* __restrict__ V, int64_t ldv,
-           int C, float* __restrict__ out, float* __restrict__ wout) {
+           int C, float* __restrict__ out, float* __restrict__ wout, int promote_every) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -156,6 +158,15 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const float* __restrict__
     const uint32_t tmem = sm.tmem_base;
 
     const int64_t cells = (int64_t)g.nx * g.ny;
+    if constexpr (PROMOTE) {
+        // the CTA's out slice holds the promoted fp32 partial sums: start from 0
+        for (int e = tid; e < TC_M * TC_TW * TC_TH; e += TC_THREADS) {
+            const int ch = cb + e / (TC_TW * TC_TH), cl = e % (TC_TW * TC_TH);
+            const int i = i0 + cl % TC_TW, j = j0 + cl / TC_TW;
+            if (ch < C && i < g.nx && j < g.ny) out[(int64_t)ch * cells + (int64_t)j * g.nx + i] = 0.0f;
+        }
+        __syncthreads();
+    }
     // dense mode: D -> fp32 partial sums in this CTA's out slice (warps 0-3, lane quarter
     // = warp), all 16 blocks; first promotion writes, later ones add
     auto promote = [&](int nprom) {
@@ -176,7 +187,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const float* __restrict__
                     const int i = bi + (n & 3), j = bj + (n >> 2);
                     if (i < g.nx && j < g.ny) {
                         float* o = out + (int64_t)ch * cells + (int64_t)j * g.nx + i;
-                        *o = (nprom > 0 ? *o : 0.0f) + __uint_as_float(r[n]);
+                        *o += __uint_as_float(r[n]);
                     }
                 }
             } else {
@@ -201,7 +212,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const float* __restrict__
         uint32_t touched = 0;
         while (walk.next(g, pd, mask, pstart, nk, row, row_change)) {
             if constexpr (PROMOTE) {
-                if (row_change && since >= PROMOTE_CHUNKS) {
+                if (since >= promote_every) {
                     // drain the tensor core, move D out (warps 0-3), restart D
                     if (lane == 0) {
                         sm.touched = touched;
@@ -366,7 +377,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const float* __restrict__
         if (warp >= 1 && warp < 4) {
             int since2 = 0;
             while (walk.next(g, pd, mask, pstart, nk, row, row_change)) {
-                if (row_change && since2 >= PROMOTE_CHUNKS) {
+                if (since2 >= promote_every) {
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     promote(prom);
                     asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -406,9 +417,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const float* __restrict__
                     if (i < g.nx && j < g.ny) {
                         float* o = out + (int64_t)ch * cells + (int64_t)j * g.nx + i;
                         float S = tb ? __uint_as_float(r[n]) : 0.0f;
-                        if constexpr (PROMOTE) {
-                            if (prom_total > 0) S += *o;
-                        }
+                        if constexpr (PROMOTE) S += *o;
                         const float W = sm.Wfin[b * TC_N + n];
                         *o = W > 0.0f ? __fdiv_rn(S, W) : qnan;
                     }
@@ -437,14 +446,18 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     dim3 grid(tiles, (C + TC_M - 1) / TC_M);
     size_t smem = sizeof(TcSmem);
     const bool dense = p->max_cand > 4096;
+    int promote_every = 32;
+    if (const char* e = getenv("HEGRID_TC_PROMOTE")) promote_every = atoi(e) > 0 ? atoi(e) : 1 << 30;
     if (dense) {
         HG_TRY(cudaFuncSetAttribute(k_accum_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
-        k_accum_tc<true><<<grid, TC_THREADS, smem, st>>>(g, p->dev(), d_v, ldv, C, d_out, d_weight);
+        k_accum_tc<true><<<grid, TC_THREADS, smem, st>>>(g, p->dev(), d_v, ldv, C, d_out, d_weight,
+                                                            promote_every);
     } else {
         HG_TRY(cudaFuncSetAttribute(k_accum_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
-        k_accum_tc<false><<<grid, TC_THREADS, smem, st>>>(g, p->dev(), d_v, ldv, C, d_out, d_weight);
+        k_accum_tc<false><<<grid, TC_THREADS, smem, st>>>(g, p->dev(), d_v, ldv, C, d_out, d_weight,
+                                                            promote_every);
     }
     count_launch();
     return cuda_status(cudaGetLastError());
