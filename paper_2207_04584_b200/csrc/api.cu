@@ -172,6 +172,8 @@ void hegrid_plan_destroy(hegrid_plan_t p) {
     cudaFree(p->d_mrow);
     cudaFree(p->d_cos_row);
     cudaFree(p->d_scratch);
+    cudaFree(p->d_tc_sched);
+    cudaFree(p->d_tc_tile_off);
     for (auto e : p->prof_events) cudaEventDestroy(e);
     delete p;
 }

@@ -71,6 +71,10 @@ struct hegrid_plan_s {
     // profiling
     bool profile = false;
     std::vector<cudaEvent_t> prof_events;  // start/stop pairs
+    // tensor-core engine: per-tile chunk schedule (built on first use, see grid_tc.cu)
+    mutable uint4* d_tc_sched = nullptr;       // {plan position, n samples, bin row, block mask}
+    mutable uint32_t* d_tc_tile_off = nullptr; // [tiles + 1]
+    mutable int64_t tc_nchunks = -1;
     // scratch for USER_CN device grids
     float* d_scratch = nullptr;
     size_t scratch_bytes = 0;
