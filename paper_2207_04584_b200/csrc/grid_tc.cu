@@ -166,7 +166,7 @@ template <bool PROMOTE>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__ sched,
            const uint32_t* __restrict__ tile_off, const float* __restrict__ V, int64_t ldv,
-           int C, float* __restrict__ out, float* __restrict__ wout, int promote_every) {
+           int C, float* __restrict__ out, float* __restrict__ wout, int promote_every, int dbg) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -253,7 +253,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
             tc::mbar_wait(&sm.a_full[sa], (c / NA) & 1);
             tc::mbar_wait(&sm.b_full[sb], (c / NBS) & 1);
             tc::fence_after_sync();
-            if (lane == 0) {
+            if (lane == 0 && !(dbg & 2)) {
                 const uint32_t bt0 = tc::smem_u32(&sm.B[sb][0]);
                 uint32_t mm = mask;
                 int q = 0;
@@ -276,6 +276,8 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                     touched |= 1u << b;
                     ++q;
                 }
+            }
+            if (lane == 0) {
                 tc::mma_commit(&sm.a_empty[sa]);
                 tc::mma_commit(&sm.b_empty[sb]);
             }
@@ -308,11 +310,12 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
         const int ch = cb + q4 * 32 + lane;
         const bool ch_ok = ch < C;
         float vn[TC_KC];
+        const bool ch_ld = ch_ok && !(dbg & 4);
         if (nchunks > 0) {
             const uint4 e = __ldg(&cs[0]);
 #pragma unroll
             for (int k = 0; k < TC_KC; ++k)
-                vn[k] = ((uint32_t)k < e.y && ch_ok) ? __ldg(V + (int64_t)(e.x + k) * ldv + ch) : 0.0f;
+                vn[k] = ((uint32_t)k < e.y && ch_ld) ? __ldg(V + (int64_t)(e.x + k) * ldv + ch) : 0.0f;
         }
         for (int c = 0; c < nchunks; ++c) {
             uint32_t hi[TC_KC], lo[TC_KC];
@@ -325,7 +328,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                 const uint4 e = __ldg(&cs[c + 1]);
 #pragma unroll
                 for (int k = 0; k < TC_KC; ++k)
-                    vn[k] = ((uint32_t)k < e.y && ch_ok) ? __ldg(V + (int64_t)(e.x + k) * ldv + ch) : 0.0f;
+                    vn[k] = ((uint32_t)k < e.y && ch_ld) ? __ldg(V + (int64_t)(e.x + k) * ldv + ch) : 0.0f;
             }
             const int sa = c % NA;
             if (c >= NA) tc::mbar_wait(&sm.a_empty[sa], ((c / NA) - 1) & 1);
@@ -366,7 +369,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
             }
             const int sb = c % NBS;
             if (c >= NBS) tc::mbar_wait(&sm.b_empty[sb], ((c / NBS) - 1) & 1);
-            const int nq = __popc(mask);
+            const int nq = (dbg & 1) ? 0 : __popc(mask);
 #pragma unroll 1
             for (int q = q0; q < nq; q += 8) {
                 const int b = __fns(mask, 0, q + 1);
@@ -490,19 +493,21 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     size_t smem = sizeof(TcSmem);
     const bool dense = p->max_cand > 4096;
     int promote_every = 16;
+    int dbg = 0;
+    if (const char* e = getenv("HEGRID_TC_DEBUG")) dbg = atoi(e);
     if (const char* e = getenv("HEGRID_TC_PROMOTE")) promote_every = atoi(e) > 0 ? atoi(e) : 1 << 30;
     if (dense) {
         HG_TRY(cudaFuncSetAttribute(k_accum_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
         k_accum_tc<true><<<grid, TC_THREADS, smem, st>>>(g, p->dev(), p->d_tc_sched,
                                                           p->d_tc_tile_off, d_v, ldv, C, d_out,
-                                                          d_weight, promote_every);
+                                                          d_weight, promote_every, dbg);
     } else {
         HG_TRY(cudaFuncSetAttribute(k_accum_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
         k_accum_tc<false><<<grid, TC_THREADS, smem, st>>>(g, p->dev(), p->d_tc_sched,
                                                            p->d_tc_tile_off, d_v, ldv, C, d_out,
-                                                           d_weight, promote_every);
+                                                           d_weight, promote_every, dbg);
     }
     count_launch();
     return cuda_status(cudaGetLastError());
