@@ -174,6 +174,7 @@ void hegrid_plan_destroy(hegrid_plan_t p) {
     cudaFree(p->d_scratch);
     cudaFree(p->d_tc_sched);
     cudaFree(p->d_tc_tile_off);
+    cudaFree(p->d_tc_wsum);
     for (auto e : p->prof_events) cudaEventDestroy(e);
     delete p;
 }

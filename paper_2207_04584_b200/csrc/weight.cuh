@@ -83,4 +83,37 @@ __device__ __forceinline__ float pair_weight(const Geom& g, const PlanDev& pd, i
     return in ? ex2_approx(d2 * g.neg_k2) : 0.0f;
 }
 
+// Weights of one sample for 4 consecutive cells (ci0 .. ci0+3) of cell row cj, sharing the
+// row terms (sin^2(dlat/2), cos products) between the 4 cells.  Same predicate as
+// pair_weight (fp32 outside the guard band, fp64 haversine inside).  ci0 is the
+// 4-aligned column of the cell block; cells >= nx and invalid samples get weight 0.
+// Used by the tensor-core engine's B producers and by the plan's W kernel, so both
+// see bit-identical weights.
+__device__ __forceinline__ void row4_weights(const Geom& g, const PlanDev& pd, int br, int cj,
+                                             int ci0, float cos_c, float4 s, uint32_t p,
+                                             bool sok, float w[4]) {
+    const float hlon = 0.5f * g.dlon_rad, hlat = 0.5f * g.dlat_rad;
+    const float dy = (float)(br - g.mlat - cj) + s.y;
+    const float a = dy * hlat;
+    const float a2 = a * a;
+    const float sa = fmaf(a2 * (-1.0f / 3.0f), a2, a2);
+    const float ccs = cos_c * s.z;
+    const float dx0 = (float)(__float_as_int(s.w) - g.mlon - ci0) + s.x;
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+        const float bb = (dx0 - (float)cc) * hlon;
+        const float b2 = bb * bb;
+        const float sbv = fmaf(b2 * (-1.0f / 3.0f), b2, b2);
+        const float h = fmaf(ccs, sbv, sa);
+        const float d2 = (4.0f * h) * fmaf(h, fmaf(h, 8.0f / 45.0f, 1.0f / 3.0f), 1.0f);
+        const bool cok = sok && (ci0 + cc < g.nx);
+        bool in = d2 <= g.R2_lo;
+        if (!in && d2 <= g.R2_hi && cok) {
+            const double2 ll = pd.ll[p];
+            in = support_fp64(g, ci0 + cc, cj, ll.x, ll.y);
+        }
+        w[cc] = (in && cok) ? ex2_approx(d2 * g.neg_k2) : 0.0f;
+    }
+}
+
 }  // namespace hg
