@@ -34,6 +34,7 @@
 //                     behind any partial sum.
 // Epilogue: tcgen05.ld of D, V = S / W (IEEE div), NaN where W = 0.
 // Deterministic: fixed chunk order, fixed work mapping, no atomics.
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <vector>
@@ -227,6 +228,11 @@ struct SchedQ {
     __device__ const uint4& peek(int k) const { return q[k]; }
 };
 
+// Debug cycle counters (HEGRID_TC_DEBUG bit 32): summed over CTAs.
+// 0 total, 1 issuer wait A, 2 issuer wait B, 3 A wait V, 4 A wait A-empty, 5 B wait B-empty,
+// 6 V wait V-empty, 7 B work, 8 A work, 9 epilogue, 10 issuer issue
+__device__ unsigned long long g_tc_prof[16];
+
 // Zero this warp's lane quarter of all accumulator columns [0, A_COL0).
 __device__ __forceinline__ void zero_d(uint32_t tmem, int q4) {
     uint32_t z[32];
@@ -248,6 +254,11 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool prof = (dbg & 32) != 0;
+    const long long t_start = clock64();
+    unsigned long long pw[4] = {0, 0, 0, 0};
+#define TPROF_BEGIN long long _t0 = prof ? clock64() : 0
+#define TPROF_END(k) if (prof) pw[k] += (unsigned long long)(clock64() - _t0)
     const int tiles_x = (g.nx + TC_TW - 1) / TC_TW;
     const int i0 = (blockIdx.x % tiles_x) * TC_TW, j0 = (blockIdx.x / tiles_x) * TC_TH;
     const int cb = blockIdx.y * TC_M;
@@ -309,9 +320,18 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                 }
             }
             const int sa = c % NA, sb = c % NBS;
-            tc::mbar_wait(&sm.a_full[sa], (c / NA) & 1);
-            tc::mbar_wait(&sm.b_full[sb], (c / NBS) & 1);
+            {
+                TPROF_BEGIN;
+                tc::mbar_wait(&sm.a_full[sa], (c / NA) & 1);
+                TPROF_END(0);
+            }
+            {
+                TPROF_BEGIN;
+                tc::mbar_wait(&sm.b_full[sb], (c / NBS) & 1);
+                TPROF_END(1);
+            }
             tc::fence_after_sync();
+            TPROF_BEGIN;
             if (lane == 0 && !(dbg & 2)) {
                 const uint32_t bt0 = tc::smem_u32(&sm.B[sb][0]);
                 uint32_t mm = mask;
@@ -339,6 +359,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                 tc::mma_commit(&sm.b_empty[sb]);
             }
             __syncwarp();
+            TPROF_END(2);
             ++since;
         }
         if (lane == 0) tc::mma_commit(&sm.bar_done);
@@ -349,7 +370,15 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
         for (int c = 0; c < nchunks; ++c) {
             const uint4 e = __ldg(&cs[c]);
             const int sv = c % NV;
-            if (c >= NV) tc::mbar_wait(&sm.v_empty[sv], ((c / NV) - 1) & 1);
+            {
+                TPROF_BEGIN;
+                if (c >= NV) tc::mbar_wait(&sm.v_empty[sv], ((c / NV) - 1) & 1);
+                TPROF_END(0);
+            }
+            if (dbg & 8) {
+                if (lane == 0) tc::mbar_arrive(&sm.v_full[sv]);
+                continue;
+            }
             if (lane == 0) tc::mbar_arrive_expect_tx(&sm.v_full[sv], e.y * row_bytes);
             __syncwarp();
             if ((uint32_t)lane < e.y)
@@ -395,7 +424,11 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                 }
             }
             const int sv = c % NV, sa = c % NA;
-            tc::mbar_wait(&sm.v_full[sv], (c / NV) & 1);
+            {
+                TPROF_BEGIN;
+                tc::mbar_wait(&sm.v_full[sv], (c / NV) & 1);
+                TPROF_END(0);
+            }
             uint32_t hi[TC_KC], lo[TC_KC];
             const float* vs = reinterpret_cast<const float*>(&sm.Vs[sv][0]) + chl;
 #pragma unroll
@@ -404,7 +437,11 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                 tc::split_tf32(v, hi[k], lo[k]);
             }
             tc::mbar_arrive(&sm.v_empty[sv]);
-            if (c >= NA) tc::mbar_wait(&sm.a_empty[sa], ((c / NA) - 1) & 1);
+            {
+                TPROF_BEGIN;
+                if (c >= NA) tc::mbar_wait(&sm.a_empty[sa], ((c / NA) - 1) & 1);
+                TPROF_END(1);
+            }
             tc::fence_after_sync();
             const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + A_COL0 + sa * 64;
             tc::tmem_st32(ta, hi);
@@ -439,7 +476,12 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                     gq[u] = (uint32_t)(4 * kq + u) < en.y ? __ldg(&pd.geo[en.x + 4 * kq + u]) : make_float4(0, 0, 0, 0);
             }
             const int sb = c % NBS;
-            if (c >= NBS) tc::mbar_wait(&sm.b_empty[sb], ((c / NBS) - 1) & 1);
+            {
+                TPROF_BEGIN;
+                if (c >= NBS) tc::mbar_wait(&sm.b_empty[sb], ((c / NBS) - 1) & 1);
+                TPROF_END(0);
+            }
+            TPROF_BEGIN;
             const int nq = (dbg & 1) ? 0 : __popc(mask);
             uint8_t* bst = &sm.B[sb][0];
 #pragma unroll 1
@@ -469,9 +511,11 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
             }
             tc::fence_proxy_async_smem();
             tc::mbar_arrive(&sm.b_full[sb]);
+            TPROF_END(1);
         }
     }
 
+    const long long t_loop = clock64();
     __syncthreads();
     // ---- epilogue: wait for the last MMAs
     tc::mbar_wait(&sm.bar_done, 0);
@@ -505,6 +549,24 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
     if (blockIdx.y == 0 && wout != nullptr && tid < TC_TW * TC_TH) {
         const int i = i0 + tid % TC_TW, j = j0 + tid / TC_TW;
         if (i < g.nx && j < g.ny) wout[(int64_t)j * g.nx + i] = __ldg(&wsum[(int64_t)j * g.nx + i]);
+    }
+    if (prof && lane == 0) {
+        const long long t_end = clock64();
+        if (warp == 0) {
+            atomicAdd(&g_tc_prof[0], (unsigned long long)(t_end - t_start));
+            atomicAdd(&g_tc_prof[1], pw[0]);
+            atomicAdd(&g_tc_prof[2], pw[1]);
+            atomicAdd(&g_tc_prof[10], pw[2]);
+            atomicAdd(&g_tc_prof[9], (unsigned long long)(t_end - t_loop));
+        } else if (warp == 4) {
+            atomicAdd(&g_tc_prof[3], pw[0]);
+            atomicAdd(&g_tc_prof[4], pw[1]);
+        } else if (warp == 8) {
+            atomicAdd(&g_tc_prof[5], pw[0]);
+            atomicAdd(&g_tc_prof[7], pw[1]);
+        } else if (warp == 1) {
+            atomicAdd(&g_tc_prof[6], pw[0]);
+        }
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -543,6 +605,19 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
                                                            dbg);
     }
     count_launch();
+    if (dbg & 32) {
+        unsigned long long h[16];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(h, g_tc_prof, sizeof(h));
+        const double tot = (double)h[0];
+        fprintf(stderr, "[tc prof] CTAs %d, cycles/CTA %.0f | issuer: waitA %.2f waitB %.2f issue %.2f | "
+                "A: waitV %.2f waitAempty %.2f | B: waitBempty %.2f work %.2f | V: waitVempty %.2f | "
+                "epilogue %.2f (fractions of CTA time)\n",
+                grid.x * grid.y, tot / (grid.x * grid.y), h[1] / tot, h[2] / tot, h[10] / tot,
+                h[3] / tot, h[4] / tot, h[5] / tot, h[7] / tot, h[6] / tot, h[9] / tot);
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
+    }
     return cuda_status(cudaGetLastError());
 }
 
