@@ -308,11 +308,11 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
         sq.init(cs, nchunks);
         int since = 0, prom = 0;
         for (int c = 0; c < nchunks; ++c) {
-            const uint32_t mask = sq.pop(c).w;
+            const uint32_t mask = __shfl_sync(0xffffffffu, sq.pop(c).w, 0);
             if constexpr (PROMOTE) {
                 if (since >= promote_every) {
                     // hand D to the A producers, wait until they have moved it out
-                    if (lane == 0) tc::mma_commit(&sm.bar_prom);
+                    tc::mma_commit_warp(&sm.bar_prom);
                     tc::mbar_wait(&sm.bar_promdone, prom & 1);
                     tc::fence_after_sync();
                     since = 0;
@@ -332,7 +332,8 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
             }
             tc::fence_after_sync();
             TPROF_BEGIN;
-            if (lane == 0 && !(dbg & 2)) {
+            if (!(dbg & 2)) {
+                // whole warp walks the runs (uniform values), one elected lane issues
                 const uint32_t bt0 = tc::smem_u32(&sm.B[sb][0]);
                 uint32_t mm = mask;
                 int q = 0;
@@ -347,22 +348,20 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                     for (int ks = 0; ks < TC_KC / 8; ++ks) {
                         const uint32_t ah = tmem + A_COL0 + sa * 64 + ks * 8;
                         const uint32_t bh = bt0 + ks * B_KS + 2 * q * 128;
-                        tc::mma_tf32_ts(d, ah, tc::sdesc(bh, B_LBO, 128), idesc, 1);
-                        tc::mma_tf32_ts(d, ah, tc::sdesc(bh + B_HALF, B_LBO, 128), idesc, 1);
-                        tc::mma_tf32_ts(d, ah + 32, tc::sdesc(bh, B_LBO, 128), idesc, 1);
+                        tc::mma_tf32_ts_warp(d, ah, tc::sdesc(bh, B_LBO, 128), idesc);
+                        tc::mma_tf32_ts_warp(d, ah, tc::sdesc(bh + B_HALF, B_LBO, 128), idesc);
+                        tc::mma_tf32_ts_warp(d, ah + 32, tc::sdesc(bh, B_LBO, 128), idesc);
                     }
                     q += r;
                 }
             }
-            if (lane == 0) {
-                tc::mma_commit(&sm.a_empty[sa]);
-                tc::mma_commit(&sm.b_empty[sb]);
-            }
+            tc::mma_commit_warp(&sm.a_empty[sa]);
+            tc::mma_commit_warp(&sm.b_empty[sb]);
             __syncwarp();
             TPROF_END(2);
             ++since;
         }
-        if (lane == 0) tc::mma_commit(&sm.bar_done);
+        tc::mma_commit_warp(&sm.bar_done);
         __syncwarp();
     } else if (warp == 1) {
         // ============================ V loader ===============================
