@@ -53,16 +53,17 @@ constexpr int TC_N = 16;                  // cells per block: 4 x 4
 constexpr int TC_TW = TC_BX * 4, TC_TH = TC_BY * 4;
 constexpr int TC_KC = 32;                 // samples per chunk (4 MMA K-steps of 8)
 constexpr int NA = 4;                     // A stages (TMEM)
-constexpr int NBS = 2;                    // B stages (SMEM)
-constexpr int NV = 4;                     // V staging stages (SMEM)
+constexpr int NBS = 4;                    // B stages (SMEM)
+constexpr int NV = 3;                     // V staging stages (SMEM)
+constexpr int MAXQ = 8;                   // max blocks (B slots) per chunk entry
 constexpr int NQ = 4;                     // schedule entries prefetched per role
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t A_COL0 = TC_NB * TC_N; // 256: A stages after the accumulators
-// B stage layout (per hi / lo half): [k-step 4][k-core 2][row group 2*16 slots][8 rows][16 B]
-constexpr uint32_t B_LBO = 2 * TC_NB * 128;          // 4096: between the 2 K core matrices
-constexpr uint32_t B_KS = 2 * B_LBO;                 // 8192: between K-steps
-constexpr uint32_t B_HALF = (TC_KC / 8) * B_KS;      // 32 KB
-constexpr uint32_t B_STAGE = 2 * B_HALF;             // 64 KB (hi + lo)
+// B stage layout (per hi / lo half): [k-step 4][k-core 2][row group 2*MAXQ slots][8 rows][16 B]
+constexpr uint32_t B_LBO = 2 * MAXQ * 128;           // 2048: between the 2 K core matrices
+constexpr uint32_t B_KS = 2 * B_LBO;                 // 4096: between K-steps
+constexpr uint32_t B_HALF = (TC_KC / 8) * B_KS;      // 16 KB
+constexpr uint32_t B_STAGE = 2 * B_HALF;             // 32 KB (hi + lo)
 constexpr int V_ROW = TC_M * 4;                      // 512 B
 constexpr int V_STAGE = TC_KC * V_ROW;               // 16 KB
 constexpr int W_THREADS = 256;            // B producers (warps 8-15)
@@ -116,12 +117,28 @@ __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int ti
                     if (rows && cols) mk |= 1u << b;
                 }
             }
-            const uint32_t bal = __ballot_sync(0xffffffffu, mk != 0);
-            if (mk && sched) {
-                const uint32_t pos = base + cnt + __popc(bal & ((1u << lane) - 1));
-                sched[pos] = make_uint4(p, n, (uint32_t)br, mk);
+            // entries per chunk: ceil(popc(mask) / MAXQ) (same samples, disjoint block sets)
+            const uint32_t ne = (__popc(mk) + MAXQ - 1) / MAXQ;
+            uint32_t incl = ne;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
             }
-            cnt += __popc(bal);
+            const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+            if (mk && sched) {
+                uint32_t pos = base + cnt + incl - ne;
+                uint32_t rest = mk;
+                while (rest) {
+                    uint32_t part = 0;
+                    for (int k = 0; k < MAXQ && rest; ++k) {
+                        part |= rest & (~rest + 1u);
+                        rest &= rest - 1;
+                    }
+                    sched[pos++] = make_uint4(p, n, (uint32_t)br, part);
+                }
+            }
+            cnt += tot;
         }
     }
     if (n_out && lane == 0) n_out[warp] = cnt;
@@ -371,7 +388,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
             const int sv = c % NV;
             {
                 TPROF_BEGIN;
-                if (c >= NV) tc::mbar_wait(&sm.v_empty[sv], ((c / NV) - 1) & 1);
+                if (c >= NV) tc::mbar_wait_sleep(&sm.v_empty[sv], ((c / NV) - 1) & 1);
                 TPROF_END(0);
             }
             if (dbg & 8) {
@@ -438,7 +455,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
             tc::mbar_arrive(&sm.v_empty[sv]);
             {
                 TPROF_BEGIN;
-                if (c >= NA) tc::mbar_wait(&sm.a_empty[sa], ((c / NA) - 1) & 1);
+                if (c >= NA) tc::mbar_wait_sleep(&sm.a_empty[sa], ((c / NA) - 1) & 1);
                 TPROF_END(1);
             }
             tc::fence_after_sync();
@@ -454,6 +471,12 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
         // ============================ B producers ============================
         const int wt = tid - 8 * 32;                  // 0..255
         const int kq = wt & 7, rr = (wt >> 3) & 3, q0 = wt >> 5;
+        float cosr[TC_BY];                        // cos(lat) of this thread's 4 possible rows
+#pragma unroll
+        for (int by = 0; by < TC_BY; ++by) {
+            const int cj = j0 + by * 4 + rr;
+            cosr[by] = cj < g.ny ? __ldg(&pd.cos_row[cj]) : 1.0f;
+        }
         SchedQ sq;
         sq.init(cs, nchunks);
         float4 gq[4];
@@ -486,10 +509,14 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
 #pragma unroll 1
             for (int q = q0; q < nq; q += 8) {
                 const int b = __fns(mask, 0, q + 1);
-                const int cj = j0 + (b / TC_BX) * 4 + rr;
+                const int by = b / TC_BX;
+                const int cj = j0 + by * 4 + rr;
                 const int ci0 = i0 + (b % TC_BX) * 4;
                 const bool rok = cj < g.ny;
-                const float cos_c = rok ? pd.cos_row[cj] : 1.0f;
+                float cos_c = cosr[0];
+#pragma unroll
+                for (int k = 1; k < TC_BY; ++k)
+                    if (by == k) cos_c = cosr[k];
                 float w[4][4];                 // [sample][cell col]
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
