@@ -518,10 +518,17 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                 for (int k = 1; k < TC_BY; ++k)
                     if (by == k) cos_c = cosr[k];
                 float w[4][4];                 // [sample][cell col]
+                if (dbg & 64) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    row4_weights(g, pd, row, cj, ci0, cos_c, g4[u], pstart + 4 * kq + u,
-                                 rok && (uint32_t)(4 * kq + u) < nk, w[u]);
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int cc = 0; cc < 4; ++cc) w[u][cc] = g4[u].x * cos_c + (float)cc;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        row4_weights(g, pd, row, cj, ci0, cos_c, g4[u], pstart + 4 * kq + u,
+                                     rok && (uint32_t)(4 * kq + u) < nk, w[u]);
+                }
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
                     const int n = rr * 4 + cc;
@@ -535,7 +542,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                     *reinterpret_cast<uint4*>(bst + B_HALF + o) = l4;
                 }
             }
-            tc::fence_proxy_async_smem();
+            if (!(dbg & 128)) tc::fence_proxy_async_smem();
             tc::mbar_arrive(&sm.b_full[sb]);
             TPROF_END(1);
         }
