@@ -15,7 +15,7 @@
 //   * the per-tile chunk schedule {plan position, n, bin row, mask of reachable blocks}
 //     (Algorithm 1's "determine the region ... of the contribution points",
 //     PAPER.md:209-217, hoisted out of the hot loop);
-//   * W per cell, summed by k_tc_wsum from the very same fp32 weights (row4_weights).
+//   * W per cell, summed by k_tc_wsum from the very same fp32 weights (patch4x4_weights).
 //
 // CTA = 16x16 cells (16 blocks) x 128 channels, 512 threads, warp-specialised:
 //   warp 0 (lane 0) : MMA issuer: per chunk, per run of consecutive in-reach blocks, 4 K-steps
@@ -84,6 +84,7 @@ __device__ __forceinline__ uint32_t b_off(int q, int n, int k) {
 
 // ------------------------------------------------------------------ plan-side pieces
 // Chunk schedule: one warp per tile; lanes evaluate 32 consecutive chunks of a row at once.
+// Entry = {plan position, n | bin row << 6, block mask, block list (4-bit nibbles, mask order)}.
 // n_out != nullptr: count only; otherwise write entries at off[tile].
 __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int tiles,
                               uint32_t* __restrict__ n_out, const uint32_t* __restrict__ off,
@@ -130,12 +131,13 @@ __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int ti
                 uint32_t pos = base + cnt + incl - ne;
                 uint32_t rest = mk;
                 while (rest) {
-                    uint32_t part = 0;
+                    uint32_t part = 0, list = 0;
                     for (int k = 0; k < MAXQ && rest; ++k) {
+                        list |= (uint32_t)(__ffs(rest) - 1) << (4 * k);
                         part |= rest & (~rest + 1u);
                         rest &= rest - 1;
                     }
-                    sched[pos++] = make_uint4(p, n, (uint32_t)br, part);
+                    sched[pos++] = make_uint4(p, n | ((uint32_t)br << 6), part, list);
                 }
             }
             cnt += tot;
@@ -144,7 +146,7 @@ __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int ti
     if (n_out && lane == 0) n_out[warp] = cnt;
 }
 
-// W per cell from the tensor-core engine's own weights (row4_weights), two-level sum
+// W per cell from the tensor-core engine's own weights (patch4x4_weights), two-level sum
 // (per bin row, then compensated) in plan order: deterministic.
 __global__ void k_tc_wsum(const __grid_constant__ Geom g, PlanDev pd, float* __restrict__ wsum) {
     const int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -159,10 +161,15 @@ __global__ void k_tc_wsum(const __grid_constant__ Geom g, PlanDev pd, float* __r
         const uint32_t s0 = pd.bin_start[rowb + i + g.mlon - m];
         const uint32_t s1 = pd.bin_start[rowb + i + g.mlon + m + 1];
         float part = 0.0f;
-        for (uint32_t s = s0; s < s1; ++s) {
-            float w[4];
-            row4_weights(g, pd, br, j, ci0, cos_c, pd.geo[s], s, true, w);
-            part += w[cc];
+        for (uint32_t s = s0; s < s1; s += 4) {
+            float4 sv[4];
+            const uint32_t nv = min(4u, s1 - s);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sv[u] = (uint32_t)u < nv ? pd.geo[s + u] : make_float4(0, 0, 0, 0);
+            float w[4][4];
+            patch4x4_weights(g, pd, br, j, ci0, cos_c, sv, s, (1u << nv) - 1u, w);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) part += w[u][cc];
         }
         const float y = part - Wc;
         const float t = W + y;
@@ -325,7 +332,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
         sq.init(cs, nchunks);
         int since = 0, prom = 0;
         for (int c = 0; c < nchunks; ++c) {
-            const uint32_t mask = __shfl_sync(0xffffffffu, sq.pop(c).w, 0);
+            const uint32_t mask = __shfl_sync(0xffffffffu, sq.pop(c).z, 0);
             if constexpr (PROMOTE) {
                 if (since >= promote_every) {
                     // hand D to the A producers, wait until they have moved it out
@@ -395,9 +402,9 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                 if (lane == 0) tc::mbar_arrive(&sm.v_full[sv]);
                 continue;
             }
-            if (lane == 0) tc::mbar_arrive_expect_tx(&sm.v_full[sv], e.y * row_bytes);
+            if (lane == 0) tc::mbar_arrive_expect_tx(&sm.v_full[sv], (e.y & 63) * row_bytes);
             __syncwarp();
-            if ((uint32_t)lane < e.y)
+            if ((uint32_t)lane < (e.y & 63))
                 tc::bulk_g2s(&sm.Vs[sv][lane * V_ROW], V + (int64_t)(e.x + lane) * ldv + cb,
                              row_bytes, &sm.v_full[sv]);
         }
@@ -449,7 +456,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
             const float* vs = reinterpret_cast<const float*>(&sm.Vs[sv][0]) + chl;
 #pragma unroll
             for (int k = 0; k < TC_KC; ++k) {
-                const float v = ((uint32_t)k < e.y && ch_ok) ? vs[k * TC_M] : 0.0f;
+                const float v = ((uint32_t)k < (e.y & 63) && ch_ok) ? vs[k * TC_M] : 0.0f;
                 tc::split_tf32(v, hi[k], lo[k]);
             }
             tc::mbar_arrive(&sm.v_empty[sv]);
@@ -484,18 +491,18 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
             const uint4 e = sq.peek(0);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                gq[u] = (uint32_t)(4 * kq + u) < e.y ? __ldg(&pd.geo[e.x + 4 * kq + u]) : make_float4(0, 0, 0, 0);
+                gq[u] = (uint32_t)(4 * kq + u) < (e.y & 63) ? __ldg(&pd.geo[e.x + 4 * kq + u]) : make_float4(0, 0, 0, 0);
         }
         for (int c = 0; c < nchunks; ++c) {
             const uint4 e = sq.pop(c);
-            const uint32_t pstart = e.x, nk = e.y, mask = e.w;
-            const int row = (int)e.z;
+            const uint32_t pstart = e.x, nk = e.y & 63, mask = e.z, blist = e.w;
+            const int row = (int)(e.y >> 6);
             float4 g4[4] = {gq[0], gq[1], gq[2], gq[3]};
             if (c + 1 < nchunks) {           // next chunk's geometry in flight
                 const uint4 en = sq.peek(0);
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
-                    gq[u] = (uint32_t)(4 * kq + u) < en.y ? __ldg(&pd.geo[en.x + 4 * kq + u]) : make_float4(0, 0, 0, 0);
+                    gq[u] = (uint32_t)(4 * kq + u) < (en.y & 63) ? __ldg(&pd.geo[en.x + 4 * kq + u]) : make_float4(0, 0, 0, 0);
             }
             const int sb = c % NBS;
             {
@@ -508,7 +515,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
             uint8_t* bst = &sm.B[sb][0];
 #pragma unroll 1
             for (int q = q0; q < nq; q += 8) {
-                const int b = __fns(mask, 0, q + 1);
+                const int b = (blist >> (4 * q)) & 15;
                 const int by = b / TC_BX;
                 const int cj = j0 + by * 4 + rr;
                 const int ci0 = i0 + (b % TC_BX) * 4;
@@ -524,10 +531,9 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
 #pragma unroll
                         for (int cc = 0; cc < 4; ++cc) w[u][cc] = g4[u].x * cos_c + (float)cc;
                 } else {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        row4_weights(g, pd, row, cj, ci0, cos_c, g4[u], pstart + 4 * kq + u,
-                                     rok && (uint32_t)(4 * kq + u) < nk, w[u]);
+                    const int nv = (int)nk - 4 * kq;
+                    const uint32_t smask = rok ? (nv >= 4 ? 15u : (nv > 0 ? (1u << nv) - 1u : 0u)) : 0u;
+                    patch4x4_weights(g, pd, row, cj, ci0, cos_c, g4, pstart + 4 * kq, smask, w);
                 }
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {

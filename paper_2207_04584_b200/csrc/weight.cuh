@@ -83,37 +83,58 @@ __device__ __forceinline__ float pair_weight(const Geom& g, const PlanDev& pd, i
     return in ? ex2_approx(d2 * g.neg_k2) : 0.0f;
 }
 
-// Weights of one sample for 4 consecutive cells (ci0 .. ci0+3) of cell row cj, sharing the
-// row terms (sin^2(dlat/2), cos products) between the 4 cells.  Same predicate as
-// pair_weight (fp32 outside the guard band, fp64 haversine inside).  ci0 is the
-// 4-aligned column of the cell block; cells >= nx and invalid samples get weight 0.
-// Used by the tensor-core engine's B producers and by the plan's W kernel, so both
-// see bit-identical weights.
-__device__ __forceinline__ void row4_weights(const Geom& g, const PlanDev& pd, int br, int cj,
-                                             int ci0, float cos_c, float4 s, uint32_t p,
-                                             bool sok, float w[4]) {
+// Weights of a 4x4 (sample x cell) patch: samples s[0..3] (plan positions p0..p0+3, valid
+// where bit u of smask is set) against 4 consecutive cells ci0 .. ci0+3 of cell row cj,
+// sharing the row terms (sin^2(dlat/2), cos products) between cells.  Same predicate as
+// pair_weight (fp32 outside the guard band, fp64 haversine inside; the rare recheck is
+// batched behind one branch).  ci0 is the 4-aligned column of the cell block; cells >= nx
+// and invalid samples get weight 0.  Used by the tensor-core engine's B producers and by
+// the plan's W kernel, so both see bit-identical weights.  w[u][cc].
+__device__ __forceinline__ void patch4x4_weights(const Geom& g, const PlanDev& pd, int br, int cj,
+                                                 int ci0, float cos_c, const float4 (&s)[4],
+                                                 uint32_t p0, uint32_t smask, float (&w)[4][4]) {
     const float hlon = 0.5f * g.dlon_rad, hlat = 0.5f * g.dlat_rad;
-    const float dy = (float)(br - g.mlat - cj) + s.y;
-    const float a = dy * hlat;
-    const float a2 = a * a;
-    const float sa = fmaf(a2 * (-1.0f / 3.0f), a2, a2);
-    const float ccs = cos_c * s.z;
-    const float dx0 = (float)(__float_as_int(s.w) - g.mlon - ci0) + s.x;
+    const uint32_t cmask = (uint32_t)(g.nx - ci0 >= 4 ? 15 : (1 << max(g.nx - ci0, 0)) - 1);
+    uint32_t rec = 0;          // bit 4u+cc: inside the guard band, needs the fp64 test
+    uint32_t inb = 0;          // bit 4u+cc: inside the support (fp32 decision)
 #pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-        const float bb = (dx0 - (float)cc) * hlon;
-        const float b2 = bb * bb;
-        const float sbv = fmaf(b2 * (-1.0f / 3.0f), b2, b2);
-        const float h = fmaf(ccs, sbv, sa);
-        const float d2 = (4.0f * h) * fmaf(h, fmaf(h, 8.0f / 45.0f, 1.0f / 3.0f), 1.0f);
-        const bool cok = sok && (ci0 + cc < g.nx);
-        bool in = d2 <= g.R2_lo;
-        if (!in && d2 <= g.R2_hi && cok) {
-            const double2 ll = pd.ll[p];
-            in = support_fp64(g, ci0 + cc, cj, ll.x, ll.y);
+    for (int u = 0; u < 4; ++u) {
+        const float dy = (float)(br - g.mlat - cj) + s[u].y;
+        const float a = dy * hlat;
+        const float a2 = a * a;
+        const float sa = fmaf(a2 * (-1.0f / 3.0f), a2, a2);
+        const float ccs = cos_c * s[u].z;
+        const float dx0 = (float)(__float_as_int(s[u].w) - g.mlon - ci0) + s[u].x;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            const float bb = (dx0 - (float)cc) * hlon;
+            const float b2 = bb * bb;
+            const float sbv = fmaf(b2 * (-1.0f / 3.0f), b2, b2);
+            const float h = fmaf(ccs, sbv, sa);
+            const float d2 = (4.0f * h) * fmaf(h, fmaf(h, 8.0f / 45.0f, 1.0f / 3.0f), 1.0f);
+            w[u][cc] = d2;
+            inb |= (d2 <= g.R2_lo ? 1u : 0u) << (4 * u + cc);
+            rec |= (d2 > g.R2_lo && d2 <= g.R2_hi ? 1u : 0u) << (4 * u + cc);
         }
-        w[cc] = (in && cok) ? ex2_approx(d2 * g.neg_k2) : 0.0f;
     }
+    uint32_t valid = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) valid |= ((smask >> u) & 1u) ? (cmask << (4 * u)) : 0u;
+    rec &= valid;
+    if (rec) {
+        while (rec) {
+            const int k = __ffs(rec) - 1;
+            rec &= rec - 1;
+            const double2 ll = pd.ll[p0 + (k >> 2)];
+            if (support_fp64(g, ci0 + (k & 3), cj, ll.x, ll.y)) inb |= 1u << k;
+        }
+    }
+    inb &= valid;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+            w[u][cc] = ((inb >> (4 * u + cc)) & 1u) ? ex2_approx(w[u][cc] * g.neg_k2) : 0.0f;
 }
 
 }  // namespace hg
