@@ -71,6 +71,7 @@ constexpr int W_THREADS = 256;            // B producers (warps 8-15)
 struct TcSmem {
     uint8_t B[NBS][B_STAGE];
     uint8_t Vs[NV][V_STAGE];
+    float4 Gs[NV][TC_KC];                 // the chunk's sample geometry (plan order)
     uint64_t a_full[NA], a_empty[NA], b_full[NBS], b_empty[NBS], v_full[NV], v_empty[NV];
     uint64_t bar_done, bar_prom, bar_promdone;
     uint32_t tmem_base;
@@ -302,7 +303,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
         }
         for (int s = 0; s < NV; ++s) {
             tc::mbar_init(&sm.v_full[s], 1);
-            tc::mbar_init(&sm.v_empty[s], 128);
+            tc::mbar_init(&sm.v_empty[s], 128 + W_THREADS);
         }
         tc::mbar_init(&sm.bar_done, 1);
         tc::mbar_init(&sm.bar_prom, 1);
@@ -357,8 +358,9 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
             tc::fence_after_sync();
             TPROF_BEGIN;
             if (!(dbg & 2)) {
-                // whole warp walks the runs (uniform values), one elected lane issues
-                const uint32_t bt0 = tc::smem_u32(&sm.B[sb][0]);
+                // whole warp walks the runs (uniform values), one elected lane issues;
+                // descriptors advance by (byte offset >> 4) in their low word
+                const uint64_t dh0 = tc::sdesc(tc::smem_u32(&sm.B[sb][0]), B_LBO, 128);
                 uint32_t mm = mask;
                 int q = 0;
                 while (mm) {
@@ -368,13 +370,14 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                     mm &= ~(((1u << r) - 1u) << b);
                     const uint32_t d = tmem + (uint32_t)(b * TC_N);
                     const uint32_t idesc = tc::idesc_tf32(TC_M, TC_N * r);
+                    const uint64_t dq = dh0 + (uint64_t)((2 * q * 128) >> 4);
+                    const uint32_t a0 = tmem + A_COL0 + sa * 64;
 #pragma unroll
                     for (int ks = 0; ks < TC_KC / 8; ++ks) {
-                        const uint32_t ah = tmem + A_COL0 + sa * 64 + ks * 8;
-                        const uint32_t bh = bt0 + ks * B_KS + 2 * q * 128;
-                        tc::mma_tf32_ts_warp(d, ah, tc::sdesc(bh, B_LBO, 128), idesc);
-                        tc::mma_tf32_ts_warp(d, ah, tc::sdesc(bh + B_HALF, B_LBO, 128), idesc);
-                        tc::mma_tf32_ts_warp(d, ah + 32, tc::sdesc(bh, B_LBO, 128), idesc);
+                        const uint64_t bh = dq + (uint64_t)((ks * B_KS) >> 4);
+                        tc::mma_tf32_ts_warp(d, a0 + ks * 8, bh, idesc);
+                        tc::mma_tf32_ts_warp(d, a0 + ks * 8, bh + (uint64_t)(B_HALF >> 4), idesc);
+                        tc::mma_tf32_ts_warp(d, a0 + 32 + ks * 8, bh, idesc);
                     }
                     q += r;
                 }
@@ -390,9 +393,20 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
     } else if (warp == 1) {
         // ============================ V loader ===============================
         const uint32_t row_bytes = (uint32_t)(((min(TC_M, C - cb) * 4) + 15) & ~15);
+        constexpr int PF = NV + 3;              // L2 prefetch distance (chunks)
+        for (int c = 0; c < PF && c < nchunks; ++c) {
+            const uint4 e = __ldg(&cs[c]);
+            if ((uint32_t)lane < (e.y & 63)) tc::prefetch_l2(V + (int64_t)(e.x + lane) * ldv + cb, row_bytes);
+        }
         for (int c = 0; c < nchunks; ++c) {
             const uint4 e = __ldg(&cs[c]);
+            const uint32_t nk = e.y & 63;
             const int sv = c % NV;
+            if (c + PF < nchunks) {
+                const uint4 ef = __ldg(&cs[c + PF]);
+                if ((uint32_t)lane < (ef.y & 63))
+                    tc::prefetch_l2(V + (int64_t)(ef.x + lane) * ldv + cb, row_bytes);
+            }
             {
                 TPROF_BEGIN;
                 if (c >= NV) tc::mbar_wait_sleep(&sm.v_empty[sv], ((c / NV) - 1) & 1);
@@ -402,11 +416,12 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                 if (lane == 0) tc::mbar_arrive(&sm.v_full[sv]);
                 continue;
             }
-            if (lane == 0) tc::mbar_arrive_expect_tx(&sm.v_full[sv], (e.y & 63) * row_bytes);
+            if (lane == 0) tc::mbar_arrive_expect_tx(&sm.v_full[sv], nk * row_bytes + nk * 16);
             __syncwarp();
-            if ((uint32_t)lane < (e.y & 63))
+            if ((uint32_t)lane < nk)
                 tc::bulk_g2s(&sm.Vs[sv][lane * V_ROW], V + (int64_t)(e.x + lane) * ldv + cb,
                              row_bytes, &sm.v_full[sv]);
+            if (lane == 0) tc::bulk_g2s(&sm.Gs[sv][0], pd.geo + e.x, nk * 16, &sm.v_full[sv]);
         }
     } else if (warp >= 4 && warp < 8) {
         // ============================ A producers ============================
@@ -486,24 +501,20 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
         }
         SchedQ sq;
         sq.init(cs, nchunks);
-        float4 gq[4];
-        if (nchunks > 0) {
-            const uint4 e = sq.peek(0);
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                gq[u] = (uint32_t)(4 * kq + u) < (e.y & 63) ? __ldg(&pd.geo[e.x + 4 * kq + u]) : make_float4(0, 0, 0, 0);
-        }
         for (int c = 0; c < nchunks; ++c) {
             const uint4 e = sq.pop(c);
             const uint32_t pstart = e.x, nk = e.y & 63, mask = e.z, blist = e.w;
             const int row = (int)(e.y >> 6);
-            float4 g4[4] = {gq[0], gq[1], gq[2], gq[3]};
-            if (c + 1 < nchunks) {           // next chunk's geometry in flight
-                const uint4 en = sq.peek(0);
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    gq[u] = (uint32_t)(4 * kq + u) < (en.y & 63) ? __ldg(&pd.geo[en.x + 4 * kq + u]) : make_float4(0, 0, 0, 0);
+            const int sv = c % NV;
+            float4 g4[4];
+            {
+                TPROF_BEGIN;
+                tc::mbar_wait(&sm.v_full[sv], (c / NV) & 1);
+                TPROF_END(2);
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) g4[u] = sm.Gs[sv][4 * kq + u];
+            tc::mbar_arrive(&sm.v_empty[sv]);
             const int sb = c % NBS;
             {
                 TPROF_BEGIN;
@@ -603,6 +614,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
         } else if (warp == 8) {
             atomicAdd(&g_tc_prof[5], pw[0]);
             atomicAdd(&g_tc_prof[7], pw[1]);
+            atomicAdd(&g_tc_prof[11], pw[2]);
         } else if (warp == 1) {
             atomicAdd(&g_tc_prof[6], pw[0]);
         }
@@ -650,10 +662,10 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
         cudaMemcpyFromSymbol(h, g_tc_prof, sizeof(h));
         const double tot = (double)h[0];
         fprintf(stderr, "[tc prof] CTAs %d, cycles/CTA %.0f | issuer: waitA %.2f waitB %.2f issue %.2f | "
-                "A: waitV %.2f waitAempty %.2f | B: waitBempty %.2f work %.2f | V: waitVempty %.2f | "
+                "A: waitV %.2f waitAempty %.2f | B: waitBempty %.2f waitV %.2f work %.2f | V: waitVempty %.2f | "
                 "epilogue %.2f (fractions of CTA time)\n",
                 grid.x * grid.y, tot / (grid.x * grid.y), h[1] / tot, h[2] / tot, h[10] / tot,
-                h[3] / tot, h[4] / tot, h[5] / tot, h[7] / tot, h[6] / tot, h[9] / tot);
+                h[3] / tot, h[4] / tot, h[5] / tot, h[11] / tot, h[7] / tot, h[6] / tot, h[9] / tot);
         unsigned long long z[16] = {0};
         cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
     }
