@@ -136,7 +136,7 @@ def user_layout_values_pinned(w, lon, lat, channel_ids, device):
     return host
 
 
-def oracle_sample(w, lon_h, lat_h, vals_h, target_s=12.0, max_cells=None):
+def oracle_sample(w, lon_h, lat_h, vals_h, target_s=15.0, max_cells=None):
     """Time the fp64 oracle (all host cores) on an evenly spaced sample of cells with all
     channels; return (throughput samples*ch/s extrapolated to the whole map, detail)."""
     import oracle
@@ -149,7 +149,13 @@ def oracle_sample(w, lon_h, lat_h, vals_h, target_s=12.0, max_cells=None):
     t0 = time.perf_counter()
     oracle.grid(lon_h, lat_h, vals_h, w.map, w.fwhm_deg, w.support, cells=cal, nthreads=nthreads)
     t_cal = time.perf_counter() - t0
-    n_cells = int(max(k, min(cells_all, k * max(1.0, target_s / max(t_cal, 1e-3)))))
+    # calibrate on a larger round (4 cells per thread) so thread start-up does not dominate
+    k2 = min(4 * nthreads, cells_all)
+    cal2 = np.linspace(0, cells_all - 1, k2).astype(np.int64)
+    t0 = time.perf_counter()
+    oracle.grid(lon_h, lat_h, vals_h, w.map, w.fwhm_deg, w.support, cells=cal2, nthreads=nthreads)
+    t_cal = time.perf_counter() - t0
+    n_cells = int(max(k2, min(cells_all, k2 * max(1.0, target_s / max(t_cal, 1e-3)))))
     if max_cells:
         n_cells = min(n_cells, max_cells)
     cells = np.linspace(0, cells_all - 1, n_cells).astype(np.int64)
@@ -307,7 +313,7 @@ def main():
             traffic = None
     roof = {"bound": "alu", "achieved": alu_achieved, "peak": fp32_peak_tflops, "unit": "TFLOP/s",
             "frac": alu_achieved / fp32_peak_tflops, "traffic": traffic,
-            "kernel": "k_accum_simt", "kernel_ms": k_avg_ms, "kernel_share": k_ms / ms_total if ms_total else None,
+            "kernel": "k_accum_tc" if args.engine == "tc" else "k_accum_simt", "kernel_ms": k_avg_ms, "kernel_share": k_ms / ms_total if ms_total else None,
             "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": alg_bytes,
             "peak_source": "148 SMs x 128 FP32 lanes x 2 flop x sm_max_mhz (DESIGN.md)"}
     hbm_roof = {"achieved": hbm_achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",

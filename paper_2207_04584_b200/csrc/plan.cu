@@ -303,7 +303,6 @@ hegrid_status build_plan(hegrid_plan_s* p, const double* d_lon, const double* d_
     cudaEvent_t e0, e1;
     HG_TRY(cudaEventCreate(&e0));
     HG_TRY(cudaEventCreate(&e1));
-    HG_TRY(cudaEventRecord(e0, st));
     size_t nn = (size_t)std::max<int64_t>(n, 1);
     HG_TRY(cudaMalloc(&p->d_keys, nn * sizeof(uint32_t)));
     HG_TRY(cudaMalloc(&p->d_perm, nn * sizeof(int32_t)));
@@ -319,6 +318,8 @@ hegrid_status build_plan(hegrid_plan_s* p, const double* d_lon, const double* d_
     int* d_bad = nullptr;
     HG_TRY(cudaMallocAsync(&d_bad, sizeof(int), st));
     HG_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+    // device time of the plan kernels only (allocations above are not part of it)
+    HG_TRY(cudaEventRecord(e0, st));
     if (n > 0) {
         int nb = (int)((n + 255) / 256);
         k_keys<<<nb, 256, 0, st>>>(g, d_lon, d_lat, n, p->d_keys, p->d_perm, d_bad);
