@@ -1,0 +1,66 @@
+"""Multi-process (gloo, world_size 2) checks of the channel-sharded N>1 host logic.
+
+On the GPU box each rank grids its own channel slice with the CUDA path; here the same
+sharding, output placement and max-over-ranks timing logic run on CPU with the oracle as
+the per-rank gridder, and the assembled result must equal a single-process run."""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2207_04584_b200.shard import channel_shard, grid_sharded
+
+
+def _worker(rank, world, port, path, C, N, out_shape):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import synth
+    w = synth.CONFIGS["cfg1"].with_(n=N, channels=C, nx=12, ny=10)
+    lon, lat = synth.coords(w)
+    vals = synth.values(w, lon, lat).numpy()
+    out = np.memmap(path, dtype=np.float64, mode="r+", shape=out_shape)
+
+    def grid_fn(v):
+        o, _, _ = oracle.grid(lon.numpy(), lat.numpy(), v, w.map, w.fwhm_deg, w.support, nthreads=1)
+        return o
+
+    grid_sharded(grid_fn, vals, world, rank, out)
+    out.flush()
+    # max-over-ranks timing reduction as bench.py does it
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    assert t.item() == float(world)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_channel_sharded_grid_equals_single_process(world):
+    import oracle
+    import synth
+    C, N = 7, 800
+    w = synth.CONFIGS["cfg1"].with_(n=N, channels=C, nx=12, ny=10)
+    shape = (C, w.cells)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "out.bin")
+        np.memmap(path, dtype=np.float64, mode="w+", shape=shape).flush()
+        port = 29500 + (os.getpid() % 2000)
+        mp.spawn(_worker, args=(world, port, path, C, N, shape), nprocs=world, join=True)
+        got = np.array(np.memmap(path, dtype=np.float64, mode="r", shape=shape))
+    lon, lat = synth.coords(w)
+    vals = synth.values(w, lon, lat).numpy()
+    ref, _, _ = oracle.grid(lon.numpy(), lat.numpy(), vals, w.map, w.fwhm_deg, w.support)
+    np.testing.assert_array_equal(np.isnan(got), np.isnan(ref))
+    np.testing.assert_array_equal(got[~np.isnan(ref)], ref[~np.isnan(ref)])
+    # every channel came from exactly one rank
+    cover = np.zeros(C, int)
+    for r in range(world):
+        a, b = channel_shard(C, world, r)
+        cover[a:b] += 1
+    assert np.all(cover == 1)
