@@ -84,6 +84,25 @@ __device__ __forceinline__ uint32_t b_off(int q, int n, int k) {
 }
 
 // ------------------------------------------------------------------ plan-side pieces
+// Can any sample in the chunk's bounding box (cells x in [xlo, xhi], y in [rc-0.5, rc+0.5])
+// be within R of any cell of the 4x4 block at (bi, bj)?  Conservative haversine lower
+// bound: sin^2(d/2) >= sin^2(dlat_min/2) + cos_min^2 sin^2(dlon_min/2).
+__device__ __forceinline__ bool block_reachable(const Geom& g, int bi, int bj, double xlo,
+                                                double xhi, int rc) {
+    const double dy = fmax(0.0, fmax((double)bj - (rc + 0.5), (rc - 0.5) - (double)(bj + 3)));
+    const double dx = fmax(0.0, fmax((double)bi - xhi, xlo - (double)(bi + 3)));
+    // latitudes involved: cell rows bj..bj+3 and the sample row extent
+    const double y0 = fmin((double)bj, rc - 0.5), y1 = fmax((double)(bj + 3), rc + 0.5);
+    const double la = g.crval_lat + (y0 + 1.0 - g.crpix_y) * g.cdelt_lat;
+    const double lb = g.crval_lat + (y1 + 1.0 - g.crpix_y) * g.cdelt_lat;
+    const double cmin = cos(fmin(89.9, fmax(fabs(la), fabs(lb))) * kDeg2Rad);
+    const double sy = sin(0.5 * dy * fabs(g.cdelt_lat) * kDeg2Rad);
+    const double sx = sin(0.5 * fmin(dx * fabs(g.cdelt_lon), 180.0) * kDeg2Rad);
+    const double hlb = sy * sy + cmin * cmin * sx * sx;
+    const double sr = sin(0.5 * g.R_rad);
+    return hlb <= sr * sr * (1.0 + 1e-6);
+}
+
 // Chunk schedule: one warp per tile; lanes evaluate 32 consecutive chunks of a row at once.
 // Entry = {plan position, n | bin row << 6, block mask, block list (4-bit nibbles, mask order)}.
 // n_out != nullptr: count only; otherwise write entries at off[tile].
@@ -111,12 +130,15 @@ __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int ti
                 n = min((uint32_t)TC_KC, s1 - p);
                 const int clo = __float_as_int(pd.geo[p].w) - g.mlon - m;
                 const int chi = __float_as_int(pd.geo[p + n - 1].w) - g.mlon + m;
+                // sample bounding box of the chunk (cell units)
+                const double xlo = __float_as_int(pd.geo[p].w) - g.mlon - 0.5;
+                const double xhi = __float_as_int(pd.geo[p + n - 1].w) - g.mlon + 0.5;
 #pragma unroll
                 for (int b = 0; b < TC_NB; ++b) {
                     const int bi = i0 + (b % TC_BX) * 4, bj = j0 + (b / TC_BX) * 4;
                     const bool rows = bj <= rc + g.rl && bj + 3 >= rc - g.rl && bj < g.ny;
                     const bool cols = bi <= chi && bi + 3 >= clo && bi < g.nx;
-                    if (rows && cols) mk |= 1u << b;
+                    if (rows && cols && block_reachable(g, bi, bj, xlo, xhi, rc)) mk |= 1u << b;
                 }
             }
             // entries per chunk: ceil(popc(mask) / MAXQ) (same samples, disjoint block sets)
@@ -166,9 +188,12 @@ __global__ void k_tc_wsum(const __grid_constant__ Geom g, PlanDev pd, float* __r
             float4 sv[4];
             const uint32_t nv = min(4u, s1 - s);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) sv[u] = (uint32_t)u < nv ? pd.geo[s + u] : make_float4(0, 0, 0, 0);
+            for (int u = 0; u < 4; ++u) {
+                sv[u] = (uint32_t)u < nv ? pd.geo[s + u] : make_float4(0, 0, 0, 0);
+                if ((uint32_t)u >= nv) sv[u].y = kInvalidDy;
+            }
             float w[4][4];
-            patch4x4_weights(g, pd, br, j, ci0, cos_c, sv, s, (1u << nv) - 1u, w);
+            patch4x4_weights(g, pd, br, j, ci0, cos_c, sv, s, w);
 #pragma unroll
             for (int u = 0; u < 4; ++u) part += w[u][cc];
         }
@@ -513,7 +538,10 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
                 TPROF_END(2);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) g4[u] = sm.Gs[sv][4 * kq + u];
+            for (int u = 0; u < 4; ++u) {
+                g4[u] = sm.Gs[sv][4 * kq + u];
+                if ((uint32_t)(4 * kq + u) >= nk) g4[u].y = kInvalidDy;
+            }
             tc::mbar_arrive(&sm.v_empty[sv]);
             const int sb = c % NBS;
             {
@@ -542,9 +570,13 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
 #pragma unroll
                         for (int cc = 0; cc < 4; ++cc) w[u][cc] = g4[u].x * cos_c + (float)cc;
                 } else {
-                    const int nv = (int)nk - 4 * kq;
-                    const uint32_t smask = rok ? (nv >= 4 ? 15u : (nv > 0 ? (1u << nv) - 1u : 0u)) : 0u;
-                    patch4x4_weights(g, pd, row, cj, ci0, cos_c, g4, pstart + 4 * kq, smask, w);
+                    patch4x4_weights(g, pd, row, cj, ci0, cos_c, g4, pstart + 4 * kq, w);
+                    if (!rok) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int cc = 0; cc < 4; ++cc) w[u][cc] = 0.0f;
+                    }
                 }
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {

@@ -83,58 +83,70 @@ __device__ __forceinline__ float pair_weight(const Geom& g, const PlanDev& pd, i
     return in ? ex2_approx(d2 * g.neg_k2) : 0.0f;
 }
 
-// Weights of a 4x4 (sample x cell) patch: samples s[0..3] (plan positions p0..p0+3, valid
-// where bit u of smask is set) against 4 consecutive cells ci0 .. ci0+3 of cell row cj,
-// sharing the row terms (sin^2(dlat/2), cos products) between cells.  Same predicate as
-// pair_weight (fp32 outside the guard band, fp64 haversine inside; the rare recheck is
-// batched behind one branch).  ci0 is the 4-aligned column of the cell block; cells >= nx
-// and invalid samples get weight 0.  Used by the tensor-core engine's B producers and by
-// the plan's W kernel, so both see bit-identical weights.  w[u][cc].
+// Weights of a 4x4 (sample x cell) patch: samples s[0..3] (plan positions p0..p0+3)
+// against 4 consecutive cells ci0 .. ci0+3 of cell row cj, sharing the per-sample terms
+// (sin^2(dlat/2), cos products, lon offset) between the 4 cells.  Same predicate as
+// pair_weight (fp32 outside the guard band, fp64 haversine inside; the rare recheck sits
+// behind one branch per patch).  Invalid samples must arrive with s.y = 1e18 (their d^2
+// is clamped to a 1-radian offset, far outside any support: weight 0); cells >= nx get
+// weight 0.  ci0 is the 4-aligned column of the
+// cell block.  Used by the tensor-core engine's B producers and by the plan's W kernel,
+// so both see bit-identical weights.  w[u][cc].
+constexpr float kInvalidDy = 1e18f;
 __device__ __forceinline__ void patch4x4_weights(const Geom& g, const PlanDev& pd, int br, int cj,
                                                  int ci0, float cos_c, const float4 (&s)[4],
-                                                 uint32_t p0, uint32_t smask, float (&w)[4][4]) {
+                                                 uint32_t p0, float (&w)[4][4]) {
     const float hlon = 0.5f * g.dlon_rad, hlat = 0.5f * g.dlat_rad;
-    const uint32_t cmask = (uint32_t)(g.nx - ci0 >= 4 ? 15 : (1 << max(g.nx - ci0, 0)) - 1);
-    uint32_t rec = 0;          // bit 4u+cc: inside the guard band, needs the fp64 test
-    uint32_t inb = 0;          // bit 4u+cc: inside the support (fp32 decision)
+    const float fy = (float)(br - g.mlat - cj);
+    const int ix = -g.mlon - ci0;
+    bool band = false;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-        const float dy = (float)(br - g.mlat - cj) + s[u].y;
-        const float a = dy * hlat;
+        const float a = fminf(fabsf((fy + s[u].y) * hlat), 1.0f);
         const float a2 = a * a;
         const float sa = fmaf(a2 * (-1.0f / 3.0f), a2, a2);
         const float ccs = cos_c * s[u].z;
-        const float dx0 = (float)(__float_as_int(s[u].w) - g.mlon - ci0) + s[u].x;
+        const float b0 = ((float)(__float_as_int(s[u].w) + ix) + s[u].x) * hlon;
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
-            const float bb = (dx0 - (float)cc) * hlon;
+            const float bb = b0 - (float)cc * hlon;
             const float b2 = bb * bb;
             const float sbv = fmaf(b2 * (-1.0f / 3.0f), b2, b2);
             const float h = fmaf(ccs, sbv, sa);
-            const float d2 = (4.0f * h) * fmaf(h, fmaf(h, 8.0f / 45.0f, 1.0f / 3.0f), 1.0f);
-            w[u][cc] = d2;
-            inb |= (d2 <= g.R2_lo ? 1u : 0u) << (4 * u + cc);
-            rec |= (d2 > g.R2_lo && d2 <= g.R2_hi ? 1u : 0u) << (4 * u + cc);
+            // 4 asin^2(sqrt h) = h (4 + 4h/3 + 32h^2/45 + ...)
+            const float d2 = h * fmaf(h, fmaf(h, 32.0f / 45.0f, 4.0f / 3.0f), 4.0f);
+            band |= (d2 > g.R2_lo) & (d2 <= g.R2_hi);
+            const float e = ex2_approx(d2 * g.neg_k2);
+            w[u][cc] = d2 <= g.R2_lo ? e : 0.0f;
         }
     }
-    uint32_t valid = 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) valid |= ((smask >> u) & 1u) ? (cmask << (4 * u)) : 0u;
-    rec &= valid;
-    if (rec) {
-        while (rec) {
-            const int k = __ffs(rec) - 1;
-            rec &= rec - 1;
-            const double2 ll = pd.ll[p0 + (k >> 2)];
-            if (support_fp64(g, ci0 + (k & 3), cj, ll.x, ll.y)) inb |= 1u << k;
+    if (band) {   // rare: decide the guard band in fp64 (recomputes the flagged pairs)
+#pragma unroll 1
+        for (int k = 0; k < 16; ++k) {
+            const int u = k >> 2, cc = k & 3;
+            const float a = fminf(fabsf((fy + s[u].y) * hlat), 1.0f);
+            const float a2 = a * a;
+            const float sa = fmaf(a2 * (-1.0f / 3.0f), a2, a2);
+            const float ccs = cos_c * s[u].z;
+            const float b0 = ((float)(__float_as_int(s[u].w) + ix) + s[u].x) * hlon;
+            const float bb = b0 - (float)cc * hlon;
+            const float b2 = bb * bb;
+            const float sbv = fmaf(b2 * (-1.0f / 3.0f), b2, b2);
+            const float h = fmaf(ccs, sbv, sa);
+            const float d2 = h * fmaf(h, fmaf(h, 32.0f / 45.0f, 4.0f / 3.0f), 4.0f);
+            if (d2 > g.R2_lo && d2 <= g.R2_hi && ci0 + cc < g.nx) {
+                const double2 ll = pd.ll[p0 + u];
+                w[u][cc] = support_fp64(g, ci0 + cc, cj, ll.x, ll.y) ? ex2_approx(d2 * g.neg_k2) : 0.0f;
+            }
         }
     }
-    inb &= valid;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
+    if (ci0 + 4 > g.nx) {
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc)
-            w[u][cc] = ((inb >> (4 * u + cc)) & 1u) ? ex2_approx(w[u][cc] * g.neg_k2) : 0.0f;
+            if (ci0 + cc >= g.nx)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) w[u][cc] = 0.0f;
+    }
 }
 
 }  // namespace hg
