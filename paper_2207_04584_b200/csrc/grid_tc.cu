@@ -189,8 +189,7 @@ __global__ void k_tc_wsum(const __grid_constant__ Geom g, PlanDev pd, float* __r
             const uint32_t nv = min(4u, s1 - s);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                sv[u] = (uint32_t)u < nv ? pd.geo[s + u] : make_float4(0, 0, 0, 0);
-                if ((uint32_t)u >= nv) sv[u].y = kInvalidDy;
+                sv[u] = (uint32_t)u < nv ? pd.geo[s + u] : make_float4(0.0f, kInvalidDy, 0.0f, 0.0f);
             }
             float w[4][4];
             patch4x4_weights(g, pd, br, j, ci0, cos_c, sv, s, w);
@@ -540,7 +539,7 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 g4[u] = sm.Gs[sv][4 * kq + u];
-                if ((uint32_t)(4 * kq + u) >= nk) g4[u].y = kInvalidDy;
+                if ((uint32_t)(4 * kq + u) >= nk) g4[u] = make_float4(0.0f, kInvalidDy, 0.0f, 0.0f);
             }
             tc::mbar_arrive(&sm.v_empty[sv]);
             const int sb = c % NBS;

@@ -87,7 +87,7 @@ __device__ __forceinline__ float pair_weight(const Geom& g, const PlanDev& pd, i
 // against 4 consecutive cells ci0 .. ci0+3 of cell row cj, sharing the per-sample terms
 // (sin^2(dlat/2), cos products, lon offset) between the 4 cells.  Same predicate as
 // pair_weight (fp32 outside the guard band, fp64 haversine inside; the rare recheck sits
-// behind one branch per patch).  Invalid samples must arrive with s.y = 1e18 (their d^2
+// behind one branch per patch).  Invalid samples must arrive as {0, 1e18, 0, 0} (their d^2
 // is clamped to a 1-radian offset, far outside any support: weight 0); cells >= nx get
 // weight 0.  ci0 is the 4-aligned column of the
 // cell block.  Used by the tensor-core engine's B producers and by the plan's W kernel,
