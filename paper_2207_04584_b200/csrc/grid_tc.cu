@@ -39,6 +39,8 @@
 
 #include <vector>
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "tc_ptx.cuh"
 #include "weight.cuh"
@@ -296,7 +298,8 @@ __device__ __forceinline__ void zero_d(uint32_t tmem, int q4) {
 // ------------------------------------------------------------------ the kernel
 template <bool PROMOTE>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__ sched,
+k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap tmap_v,
+           PlanDev pd, const uint4* __restrict__ sched,
            const uint32_t* __restrict__ tile_off, const float* __restrict__ wsum,
            const float* __restrict__ V, int64_t ldv, int C, float* __restrict__ out,
            float* __restrict__ wout, int promote_every, int dbg) {
@@ -416,37 +419,31 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
         __syncwarp();
     } else if (warp == 1) {
         // ============================ V loader ===============================
-        const uint32_t row_bytes = (uint32_t)(((min(TC_M, C - cb) * 4) + 15) & ~15);
-        constexpr int PF = NV + 3;              // L2 prefetch distance (chunks)
-        for (int c = 0; c < PF && c < nchunks; ++c) {
-            const uint4 e = __ldg(&cs[c]);
-            if ((uint32_t)lane < (e.y & 63)) tc::prefetch_l2(V + (int64_t)(e.x + lane) * ldv + cb, row_bytes);
+        // one 2D TMA box (32 plan rows x 128 channels, out-of-range rows/channels zero) and
+        // one bulk copy of the 32 geometry records per chunk, L2 prefetch PF chunks ahead
+        constexpr int PF = NV + 3;
+        if (lane == 0) {
+            for (int c = 0; c < PF && c < nchunks; ++c) tc::tma_prefetch_2d(&tmap_v, cb, (int)__ldg(&cs[c].x));
+            for (int c = 0; c < nchunks; ++c) {
+                const uint4 e = __ldg(&cs[c]);
+                const uint32_t nk = e.y & 63;
+                const int sv = c % NV;
+                if (c + PF < nchunks) tc::tma_prefetch_2d(&tmap_v, cb, (int)__ldg(&cs[c + PF].x));
+                {
+                    TPROF_BEGIN;
+                    if (c >= NV) tc::mbar_wait_sleep(&sm.v_empty[sv], ((c / NV) - 1) & 1);
+                    TPROF_END(0);
+                }
+                if (dbg & 8) {
+                    tc::mbar_arrive(&sm.v_full[sv]);
+                    continue;
+                }
+                tc::mbar_arrive_expect_tx(&sm.v_full[sv], (uint32_t)V_STAGE + nk * 16);
+                tc::tma_load_2d(&sm.Vs[sv][0], &tmap_v, cb, (int)e.x, &sm.v_full[sv]);
+                tc::bulk_g2s(&sm.Gs[sv][0], pd.geo + e.x, nk * 16, &sm.v_full[sv]);
+            }
         }
-        for (int c = 0; c < nchunks; ++c) {
-            const uint4 e = __ldg(&cs[c]);
-            const uint32_t nk = e.y & 63;
-            const int sv = c % NV;
-            if (c + PF < nchunks) {
-                const uint4 ef = __ldg(&cs[c + PF]);
-                if ((uint32_t)lane < (ef.y & 63))
-                    tc::prefetch_l2(V + (int64_t)(ef.x + lane) * ldv + cb, row_bytes);
-            }
-            {
-                TPROF_BEGIN;
-                if (c >= NV) tc::mbar_wait_sleep(&sm.v_empty[sv], ((c / NV) - 1) & 1);
-                TPROF_END(0);
-            }
-            if (dbg & 8) {
-                if (lane == 0) tc::mbar_arrive(&sm.v_full[sv]);
-                continue;
-            }
-            if (lane == 0) tc::mbar_arrive_expect_tx(&sm.v_full[sv], nk * row_bytes + nk * 16);
-            __syncwarp();
-            if ((uint32_t)lane < nk)
-                tc::bulk_g2s(&sm.Vs[sv][lane * V_ROW], V + (int64_t)(e.x + lane) * ldv + cb,
-                             row_bytes, &sm.v_full[sv]);
-            if (lane == 0) tc::bulk_g2s(&sm.Gs[sv][0], pd.geo + e.x, nk * 16, &sm.v_full[sv]);
-        }
+        __syncwarp();
     } else if (warp >= 4 && warp < 8) {
         // ============================ A producers ============================
         const int q4 = warp & 3;
@@ -655,12 +652,40 @@ k_accum_tc(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__
     if (warp == 0) tc::tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+static hegrid_status make_value_tmap(CUtensorMap* tm, const float* d_v, int64_t ldv, int C,
+                                     int64_t rows) {
+    using encode_fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static encode_fn fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !f)
+            return HEGRID_ECUDA;
+        fn = (encode_fn)f;
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)std::max<int64_t>(rows, 1)};
+    const cuuint64_t strides[1] = {(cuuint64_t)ldv * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)TC_M, (cuuint32_t)TC_KC};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)d_v, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? HEGRID_OK : HEGRID_EINVAL;
+}
+
 hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int64_t ldv,
                                    int64_t n_channels, float* d_out, float* d_weight,
                                    cudaStream_t st) {
     if (n_channels <= 0) return HEGRID_OK;
     if (n_channels > (1LL << 30)) return HEGRID_EINVAL;
     HG_TRY_S(ensure_tc_plan(p, st));
+    alignas(64) CUtensorMap tmap;
+    HG_TRY_S(make_value_tmap(&tmap, d_v, ldv, (int)n_channels, p->n_used));
     const Geom& g = p->g;
     int C = (int)n_channels;
     int tiles = ((g.nx + TC_TW - 1) / TC_TW) * ((g.ny + TC_TH - 1) / TC_TH);
@@ -674,14 +699,14 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     if (dense) {
         HG_TRY(cudaFuncSetAttribute(k_accum_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
-        k_accum_tc<true><<<grid, TC_THREADS, smem, st>>>(g, p->dev(), p->d_tc_sched,
+        k_accum_tc<true><<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched,
                                                           p->d_tc_tile_off, p->d_tc_wsum, d_v,
                                                           ldv, C, d_out, d_weight, promote_every,
                                                           dbg);
     } else {
         HG_TRY(cudaFuncSetAttribute(k_accum_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
-        k_accum_tc<false><<<grid, TC_THREADS, smem, st>>>(g, p->dev(), p->d_tc_sched,
+        k_accum_tc<false><<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched,
                                                            p->d_tc_tile_off, p->d_tc_wsum, d_v,
                                                            ldv, C, d_out, d_weight, promote_every,
                                                            dbg);
