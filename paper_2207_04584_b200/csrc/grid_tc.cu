@@ -77,6 +77,7 @@ struct TcSmem {
     uint64_t a_full[NA], a_empty[NA], b_full[NBS], b_empty[NBS], v_full[NV], v_empty[NV];
     uint64_t bar_done, bar_prom, bar_promdone;
     uint32_t tmem_base;
+    uint32_t touched;
 };
 
 // byte offset of (slot q, cell n, sample k) inside one half (hi or lo) of a B stage
@@ -333,7 +334,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             tc::mbar_init(&sm.v_empty[s], 128 + W_THREADS);
         }
         tc::mbar_init(&sm.bar_done, 1);
-        tc::mbar_init(&sm.bar_prom, 1);
+        tc::mbar_init(&sm.bar_prom, 2);   // MMA commit + issuer's release arrive (touched)
         tc::mbar_init(&sm.bar_promdone, 128);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -359,14 +360,19 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         SchedQ sq;
         sq.init(cs, nchunks);
         int since = 0, prom = 0;
+        uint32_t touched = 0xFFFFu;         // D starts zeroed: every block accumulates
         for (int c = 0; c < nchunks; ++c) {
             const uint32_t mask = __shfl_sync(0xffffffffu, sq.pop(c).z, 0);
             if constexpr (PROMOTE) {
                 if (since >= promote_every) {
                     // hand D to the A producers, wait until they have moved it out
+                    sm.touched = touched;
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(&sm.bar_prom);
                     tc::mma_commit_warp(&sm.bar_prom);
                     tc::mbar_wait(&sm.bar_promdone, prom & 1);
                     tc::fence_after_sync();
+                    touched = 0;                // next MMA on each block overwrites D
                     since = 0;
                     ++prom;
                 }
@@ -391,9 +397,11 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 uint32_t mm = mask;
                 int q = 0;
                 while (mm) {
-                    // run of consecutive in-reach blocks [b, b + r)
+                    // run of consecutive in-reach blocks [b, b + r) with the same D state
                     const int b = __ffs(mm) - 1;
-                    const int r = __ffs(~(mm >> b)) - 1;
+                    const uint32_t tb = (touched >> b) & 1u;
+                    const uint32_t same = mm & (tb ? touched : ~touched);
+                    const int r = __ffs(~(same >> b)) - 1;
                     mm &= ~(((1u << r) - 1u) << b);
                     const uint32_t d = tmem + (uint32_t)(b * TC_N);
                     const uint32_t idesc = tc::idesc_tf32(TC_M, TC_N * r);
@@ -402,10 +410,11 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 #pragma unroll
                     for (int ks = 0; ks < TC_KC / 8; ++ks) {
                         const uint64_t bh = dq + (uint64_t)((ks * B_KS) >> 4);
-                        tc::mma_tf32_ts_warp(d, a0 + ks * 8, bh, idesc);
+                        tc::mma_tf32_ts_warp_acc(d, a0 + ks * 8, bh, idesc, (ks > 0) | tb);
                         tc::mma_tf32_ts_warp(d, a0 + ks * 8, bh + (uint64_t)(B_HALF >> 4), idesc);
                         tc::mma_tf32_ts_warp(d, a0 + 32 + ks * 8, bh, idesc);
                     }
+                    touched |= ((1u << r) - 1u) << b;
                     q += r;
                 }
             }
@@ -415,6 +424,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             TPROF_END(2);
             ++since;
         }
+        sm.touched = touched;
         tc::mma_commit_warp(&sm.bar_done);
         __syncwarp();
     } else if (warp == 1) {
@@ -460,8 +470,10 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     tc::mbar_wait(&sm.bar_prom, prom & 1);
                     tc::fence_after_sync();
                     const int ch = cb + chl;
+                    const uint32_t tm = *(volatile uint32_t*)&sm.touched;
 #pragma unroll 1
                     for (int b = 0; b < TC_NB; ++b) {
+                        if (!((tm >> b) & 1u)) continue;
                         uint32_t r[16];
                         tc::tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * TC_N), r);
                         tc::wait_ld();
@@ -475,7 +487,6 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                             }
                         }
                     }
-                    zero_d(tmem, q4);
                     tc::fence_before_sync();
                     tc::mbar_arrive(&sm.bar_promdone);
                     since = 0;
@@ -606,6 +617,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         for (int a = 0; a < 8; ++a) {
             const int b = half * 8 + a;
             uint32_t r[16];
+            const bool tb = (sm.touched >> b) & 1u;
             tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(b * TC_N), r);
             tc::wait_ld();
             if (ch < C) {
@@ -615,7 +627,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     const int i = bi + (n & 3), j = bj + (n >> 2);
                     if (i < g.nx && j < g.ny) {
                         float* o = out + (int64_t)ch * cells + (int64_t)j * g.nx + i;
-                        float S = __uint_as_float(r[n]);
+                        float S = tb ? __uint_as_float(r[n]) : 0.0f;
                         if constexpr (PROMOTE) S += *o;
                         const float W = __ldg(&wsum[(int64_t)j * g.nx + i]);
                         *o = W > 0.0f ? __fdiv_rn(S, W) : qnan;
