@@ -703,7 +703,8 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     int tiles = ((g.nx + TC_TW - 1) / TC_TW) * ((g.ny + TC_TH - 1) / TC_TH);
     dim3 grid(tiles, (C + TC_M - 1) / TC_M);
     size_t smem = sizeof(TcSmem);
-    const bool dense = p->max_cand > 4096;
+    bool dense = p->max_cand > 4096;
+    if (const char* e = getenv("HEGRID_TC_DENSE")) dense = atoi(e) != 0;
     int promote_every = 16;
     if (const char* e = getenv("HEGRID_TC_PROMOTE")) promote_every = atoi(e) > 0 ? atoi(e) : 1 << 30;
     int dbg = 0;
