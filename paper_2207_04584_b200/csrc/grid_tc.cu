@@ -75,7 +75,7 @@ struct TcSmem {
     uint8_t Vs[NV][V_STAGE];
     float4 Gs[NV][TC_KC];                 // the chunk's sample geometry (plan order)
     uint64_t a_full[NA], a_empty[NA], b_full[NBS], b_empty[NBS], v_full[NV], v_empty[NV];
-    uint64_t bar_done, bar_prom, bar_promdone;
+    uint64_t bar_done, bar_prom, bar_promdone, bar_drain;
     uint32_t tmem_base;
     uint32_t touched;
 };
@@ -334,7 +334,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             tc::mbar_init(&sm.v_empty[s], 128 + W_THREADS);
         }
         tc::mbar_init(&sm.bar_done, 1);
-        tc::mbar_init(&sm.bar_prom, 2);   // MMA commit + issuer's release arrive (touched)
+        tc::mbar_init(&sm.bar_prom, 1);
+        tc::mbar_init(&sm.bar_drain, 1);
         tc::mbar_init(&sm.bar_promdone, 128);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -366,10 +367,15 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             if constexpr (PROMOTE) {
                 if (since >= promote_every) {
                     // hand D to the A producers, wait until they have moved it out
+                    // drain: the issuer itself waits for all its MMAs, then releases the
+                    // A producers with a plain arrive (touched mask published with it)
+                    tc::mma_commit_warp(&sm.bar_drain);
+                    tc::mbar_wait(&sm.bar_drain, prom & 1);
+                    tc::fence_after_sync();
                     sm.touched = touched;
+                    tc::fence_before_sync();
                     __syncwarp();
                     if (lane == 0) tc::mbar_arrive(&sm.bar_prom);
-                    tc::mma_commit_warp(&sm.bar_prom);
                     tc::mbar_wait(&sm.bar_promdone, prom & 1);
                     tc::fence_after_sync();
                     touched = 0;                // next MMA on each block overwrites D
