@@ -378,7 +378,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     if (lane == 0) tc::mbar_arrive(&sm.bar_prom);
                     tc::mbar_wait(&sm.bar_promdone, prom & 1);
                     tc::fence_after_sync();
-                    touched = 0;                // next MMA on each block overwrites D
+                    touched = (dbg & 256) ? 0xFFFFu : 0u;   // next MMA on each block overwrites D
                     since = 0;
                     ++prom;
                 }
@@ -493,6 +493,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                             }
                         }
                     }
+                    if (dbg & 256) zero_d(tmem, q4);
                     tc::fence_before_sync();
                     tc::mbar_arrive(&sm.bar_promdone);
                     since = 0;
