@@ -472,7 +472,10 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const uint4 e = sq.pop(c);
             if constexpr (PROMOTE) {
                 if (since >= promote_every) {
-                    // D -> out slice (this warp's lane quarter, all touched blocks)
+                    // D -> out slice (this warp's lane quarter, all touched blocks).  The
+                    // four A warps enter together so none can run a whole promotion ahead
+                    // (parity waits alias across two phases).
+                    asm volatile("bar.sync 3, 128;" ::: "memory");
                     tc::mbar_wait(&sm.bar_prom, prom & 1);
                     tc::fence_after_sync();
                     const int ch = cb + chl;
