@@ -620,12 +620,15 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     tc::mbar_wait(&sm.bar_done, 0);
     tc::fence_after_sync();
     const float qnan = __int_as_float(0x7fc00000);
-    if (warp < 8) {
+    // epilogue warps: in dense mode the A warps (4-7), which also own the promoted partial
+    // sums of their channels, each take all 16 blocks; otherwise warps 0-7 split them
+    const bool epi = PROMOTE ? (warp >= 4 && warp < 8) : (warp < 8);
+    if (epi) {
         const int ch = cb + (warp & 3) * 32 + lane;
-        const int half = warp >> 2;
+        const int a_lo = PROMOTE ? 0 : (warp >> 2) * 8;
+        const int a_hi = PROMOTE ? TC_NB : a_lo + 8;
 #pragma unroll 1
-        for (int a = 0; a < 8; ++a) {
-            const int b = half * 8 + a;
+        for (int b = a_lo; b < a_hi; ++b) {
             uint32_t r[16];
             const bool tb = (sm.touched >> b) & 1u;
             tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(b * TC_N), r);
