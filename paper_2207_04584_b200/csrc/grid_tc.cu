@@ -486,6 +486,16 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                         uint32_t r[16];
                         tc::tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * TC_N), r);
                         tc::wait_ld();
+                        if (dbg & 512) {     // debug: is D still changing during the promotion?
+                            __nanosleep(5000);
+                            uint32_t r2[16];
+                            tc::tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * TC_N), r2);
+                            tc::wait_ld();
+                            int nd = 0;
+#pragma unroll
+                            for (int n = 0; n < 16; ++n) nd += r2[n] != r[n];
+                            if (nd) atomicAdd(&g_tc_prof[12], (unsigned long long)nd);
+                        }
                         if (ch < C) {
                             const int bi = i0 + (b % TC_BX) * 4, bj = j0 + (b / TC_BX) * 4;
 #pragma unroll
@@ -748,6 +758,7 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
                 "epilogue %.2f (fractions of CTA time)\n",
                 grid.x * grid.y, tot / (grid.x * grid.y), h[1] / tot, h[2] / tot, h[10] / tot,
                 h[3] / tot, h[4] / tot, h[5] / tot, h[11] / tot, h[7] / tot, h[6] / tot, h[9] / tot);
+        fprintf(stderr, "[tc prof] D changed during promotion reads: %llu\n", h[12]);
         unsigned long long z[16] = {0};
         cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
     }
