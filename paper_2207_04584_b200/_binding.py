@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhegrid.so")
+LIB_PATH = os.environ.get("HEGRID_LIB") or os.path.join(_HERE, "libhegrid.so")
 
 HEGRID_OK = 0
 STATUS = {0: "HEGRID_OK", 1: "HEGRID_EINVAL", 2: "HEGRID_EDOMAIN", 3: "HEGRID_ENOMEM",

@@ -54,9 +54,18 @@ constexpr int TC_NB = TC_BX * TC_BY;      // 16 blocks
 constexpr int TC_N = 16;                  // cells per block: 4 x 4
 constexpr int TC_TW = TC_BX * 4, TC_TH = TC_BY * 4;
 constexpr int TC_KC = 32;                 // samples per chunk (4 MMA K-steps of 8)
-constexpr int NA = 4;                     // A stages (TMEM)
-constexpr int NBS = 4;                    // B stages (SMEM)
-constexpr int NV = 3;                     // V staging stages (SMEM)
+#ifndef HG_TC_NA
+#define HG_TC_NA 4
+#endif
+#ifndef HG_TC_NBS
+#define HG_TC_NBS 4
+#endif
+#ifndef HG_TC_NV
+#define HG_TC_NV 3
+#endif
+constexpr int NA = HG_TC_NA;              // A stages (TMEM)
+constexpr int NBS = HG_TC_NBS;            // B stages (SMEM)
+constexpr int NV = HG_TC_NV;              // V staging stages (SMEM)
 constexpr int MAXQ = 8;                   // max blocks (B slots) per chunk entry
 constexpr int NQ = 4;                     // schedule entries prefetched per role
 constexpr uint32_t TMEM_COLS = 512;
