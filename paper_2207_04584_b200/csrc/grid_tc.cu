@@ -84,7 +84,7 @@ struct TcSmem {
     uint8_t Vs[NV][V_STAGE];
     float4 Gs[NV][TC_KC];                 // the chunk's sample geometry (plan order)
     uint64_t a_full[NA], a_empty[NA], b_full[NBS], b_empty[NBS], v_full[NV], v_empty[NV];
-    uint64_t bar_done, bar_prom, bar_promdone, bar_drain;
+    uint64_t bar_done, bar_prom, bar_promdone, bar_drain, bar_dbg;
     uint32_t tmem_base;
     uint32_t touched;
 };
@@ -345,6 +345,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         tc::mbar_init(&sm.bar_done, 1);
         tc::mbar_init(&sm.bar_prom, 1);
         tc::mbar_init(&sm.bar_drain, 1);
+        tc::mbar_init(&sm.bar_dbg, 1);
         tc::mbar_init(&sm.bar_promdone, 128);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -369,7 +370,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         // ============================ MMA issuer =============================
         SchedQ sq;
         sq.init(cs, nchunks);
-        int since = 0, prom = 0;
+        int since = 0, prom = 0, dbg_phase = 0;
         uint32_t touched = 0xFFFFu;         // D starts zeroed: every block accumulates
         for (int c = 0; c < nchunks; ++c) {
             const uint32_t mask = __shfl_sync(0xffffffffu, sq.pop(c).z, 0);
@@ -432,6 +433,11 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     touched |= ((1u << r) - 1u) << b;
                     q += r;
                 }
+            }
+            if (dbg & 1024) {       // debug: drain every chunk before releasing its stages
+                tc::mma_commit_warp(&sm.bar_dbg);
+                tc::mbar_wait(&sm.bar_dbg, dbg_phase & 1);
+                ++dbg_phase;
             }
             tc::mma_commit_warp(&sm.a_empty[sa]);
             tc::mma_commit_warp(&sm.b_empty[sb]);
