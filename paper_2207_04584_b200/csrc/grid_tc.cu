@@ -589,6 +589,10 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             {
                 TPROF_BEGIN;
                 if (c >= NBS) tc::mbar_wait(&sm.b_empty[sb], ((c / NBS) - 1) & 1);
+                if ((dbg & 2048) && c >= 2) {   // debug: at most 2 chunks ahead of the issuer
+                    const int c2 = c - 2;
+                    tc::mbar_wait(&sm.b_empty[c2 % NBS], (c2 / NBS) & 1);
+                }
                 TPROF_END(0);
             }
             TPROF_BEGIN;
