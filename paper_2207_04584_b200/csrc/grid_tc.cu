@@ -57,11 +57,15 @@ constexpr int TC_KC = 32;                 // samples per chunk (4 MMA K-steps of
 #ifndef HG_TC_NA
 #define HG_TC_NA 4
 #endif
+// NBS = 2: with 3-4 weight stages (producers up to 3 chunks ahead of the tensor core)
+// results became timing-dependent although every stage handoff is mbarrier-ordered; the
+// cause is not yet understood (tools/det_small.py reproduces it), so the
+// engine runs with 2 weight stages, which is deterministic in every test.
 #ifndef HG_TC_NBS
-#define HG_TC_NBS 4
+#define HG_TC_NBS 2
 #endif
 #ifndef HG_TC_NV
-#define HG_TC_NV 3
+#define HG_TC_NV 5
 #endif
 constexpr int NA = HG_TC_NA;              // A stages (TMEM)
 constexpr int NBS = HG_TC_NBS;            // B stages (SMEM)
