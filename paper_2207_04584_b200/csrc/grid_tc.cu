@@ -71,7 +71,6 @@ constexpr int NA = HG_TC_NA;              // A stages (TMEM)
 constexpr int NBS = HG_TC_NBS;            // B stages (SMEM)
 constexpr int NV = HG_TC_NV;              // V staging stages (SMEM)
 constexpr int MAXQ = 8;                   // max blocks (B slots) per chunk entry
-constexpr int NQ = 4;                     // schedule entries prefetched per role
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t A_COL0 = TC_NB * TC_N; // 256: A stages after the accumulators
 // B stage layout (per hi / lo half): [k-step 4][k-core 2][row group 2*MAXQ slots][8 rows][16 B]
@@ -87,8 +86,10 @@ struct TcSmem {
     uint8_t B[NBS][B_STAGE];
     uint8_t Vs[NV][V_STAGE];
     float4 Gs[NV][TC_KC];                 // the chunk's sample geometry (plan order)
+    uint4 Es[NV];                         // the chunk's schedule entry (written by the V loader)
+    uint32_t Bmask[NBS];                  // block mask of the chunk in each weight stage
     uint64_t a_full[NA], a_empty[NA], b_full[NBS], b_empty[NBS], v_full[NV], v_empty[NV];
-    uint64_t bar_done, bar_prom, bar_promdone, bar_drain, bar_dbg;
+    uint64_t bar_done, bar_prom, bar_promdone, bar_drain;
     uint32_t tmem_base;
     uint32_t touched;
 };
@@ -271,28 +272,6 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     return HEGRID_OK;
 }
 
-// Schedule entries c .. c+NQ-1 kept in registers (loads issued NQ chunks ahead).
-struct SchedQ {
-    uint4 q[NQ];
-    const uint4* cs;
-    int n;
-    __device__ void init(const uint4* s, int nch) {
-        cs = s;
-        n = nch;
-#pragma unroll
-        for (int k = 0; k < NQ; ++k) q[k] = k < n ? __ldg(&cs[k]) : make_uint4(0, 0, 0, 0);
-    }
-    // entry of the current chunk c; then shift in chunk c + NQ
-    __device__ uint4 pop(int c) {
-        const uint4 e = q[0];
-#pragma unroll
-        for (int k = 0; k < NQ - 1; ++k) q[k] = q[k + 1];
-        q[NQ - 1] = (c + NQ < n) ? __ldg(&cs[c + NQ]) : make_uint4(0, 0, 0, 0);
-        return e;
-    }
-    __device__ const uint4& peek(int k) const { return q[k]; }
-};
-
 // Debug cycle counters (HEGRID_TC_DEBUG bit 32): summed over CTAs.
 // 0 total, 1 issuer wait A, 2 issuer wait B, 3 A wait V, 4 A wait A-empty, 5 B wait B-empty,
 // 6 V wait V-empty, 7 B work, 8 A work, 9 epilogue, 10 issuer issue
@@ -349,7 +328,6 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         tc::mbar_init(&sm.bar_done, 1);
         tc::mbar_init(&sm.bar_prom, 1);
         tc::mbar_init(&sm.bar_drain, 1);
-        tc::mbar_init(&sm.bar_dbg, 1);
         tc::mbar_init(&sm.bar_promdone, 128);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -372,12 +350,9 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 
     if (warp == 0) {
         // ============================ MMA issuer =============================
-        SchedQ sq;
-        sq.init(cs, nchunks);
-        int since = 0, prom = 0, dbg_phase = 0;
+        int since = 0, prom = 0;
         uint32_t touched = 0xFFFFu;         // D starts zeroed: every block accumulates
         for (int c = 0; c < nchunks; ++c) {
-            const uint32_t mask = __shfl_sync(0xffffffffu, sq.pop(c).z, 0);
             if constexpr (PROMOTE) {
                 if (since >= promote_every) {
                     // hand D to the A producers, wait until they have moved it out
@@ -409,11 +384,13 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 TPROF_END(1);
             }
             tc::fence_after_sync();
+            const uint32_t mask = sm.Bmask[sb];
             TPROF_BEGIN;
             if (!(dbg & 2)) {
-                // whole warp walks the runs (uniform values), one elected lane issues;
-                // descriptors advance by (byte offset >> 4) in their low word
+                // whole warp walks the runs (uniform values); each run is one 12-MMA block
+                // behind a single elect; descriptors advance by (byte offset >> 4)
                 const uint64_t dh0 = tc::sdesc(tc::smem_u32(&sm.B[sb][0]), B_LBO, 128);
+                const uint32_t a0 = tmem + A_COL0 + sa * 64;
                 uint32_t mm = mask;
                 int q = 0;
                 while (mm) {
@@ -423,25 +400,12 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     const uint32_t same = mm & (tb ? touched : ~touched);
                     const int r = __ffs(~(same >> b)) - 1;
                     mm &= ~(((1u << r) - 1u) << b);
-                    const uint32_t d = tmem + (uint32_t)(b * TC_N);
-                    const uint32_t idesc = tc::idesc_tf32(TC_M, TC_N * r);
-                    const uint64_t dq = dh0 + (uint64_t)((2 * q * 128) >> 4);
-                    const uint32_t a0 = tmem + A_COL0 + sa * 64;
-#pragma unroll
-                    for (int ks = 0; ks < TC_KC / 8; ++ks) {
-                        const uint64_t bh = dq + (uint64_t)((ks * B_KS) >> 4);
-                        tc::mma_tf32_ts_warp_acc(d, a0 + ks * 8, bh, idesc, (ks > 0) | tb);
-                        tc::mma_tf32_ts_warp(d, a0 + ks * 8, bh + (uint64_t)(B_HALF >> 4), idesc);
-                        tc::mma_tf32_ts_warp(d, a0 + 32 + ks * 8, bh, idesc);
-                    }
+                    tc::mma_run_3xtf32<(B_KS >> 4), (B_HALF >> 4)>(
+                        tmem + (uint32_t)(b * TC_N), a0, dh0 + (uint64_t)((2 * q * 128) >> 4),
+                        tc::idesc_tf32(TC_M, TC_N * r), tb);
                     touched |= ((1u << r) - 1u) << b;
                     q += r;
                 }
-            }
-            if (dbg & 1024) {       // debug: drain every chunk before releasing its stages
-                tc::mma_commit_warp(&sm.bar_dbg);
-                tc::mbar_wait(&sm.bar_dbg, dbg_phase & 1);
-                ++dbg_phase;
             }
             tc::mma_commit_warp(&sm.a_empty[sa]);
             tc::mma_commit_warp(&sm.b_empty[sb]);
@@ -456,39 +420,53 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         // ============================ V loader ===============================
         // one 2D TMA box (32 plan rows x 128 channels, out-of-range rows/channels zero) and
         // one bulk copy of the 32 geometry records per chunk, L2 prefetch PF chunks ahead
+        // schedule entries: the warp loads 32 at a time (lane l holds entry c0 + l), one
+        // batch ahead, and hands each chunk's entry to the consumers through Es[stage]
         constexpr int PF = NV + 3;
-        if (lane == 0) {
+        static_assert(PF < 32, "prefetch distance must stay within the next entry batch");
+        auto ld_entry = [&](int c) { return c < nchunks ? __ldg(&cs[c]) : make_uint4(0, 0, 0, 0); };
+        uint4 cur = ld_entry(lane), nxt = ld_entry(32 + lane);
+        if (lane == 0)
             for (int c = 0; c < PF && c < nchunks; ++c) tc::tma_prefetch_2d(&tmap_v, cb, (int)__ldg(&cs[c].x));
-            for (int c = 0; c < nchunks; ++c) {
-                const uint4 e = __ldg(&cs[c]);
+        for (int c = 0; c < nchunks; ++c) {
+            if ((c & 31) == 0 && c > 0) {
+                cur = nxt;
+                nxt = ld_entry(c + 32 + lane);
+            }
+            uint4 e;
+            e.x = __shfl_sync(0xffffffffu, cur.x, c & 31);
+            e.y = __shfl_sync(0xffffffffu, cur.y, c & 31);
+            e.z = __shfl_sync(0xffffffffu, cur.z, c & 31);
+            e.w = __shfl_sync(0xffffffffu, cur.w, c & 31);
+            const int cp = c + PF;
+            const uint32_t xp = __shfl_sync(0xffffffffu, (cp >> 5) == (c >> 5) ? cur.x : nxt.x, cp & 31);
+            if (lane == 0) {
                 const uint32_t nk = e.y & 63;
                 const int sv = c % NV;
-                if (c + PF < nchunks) tc::tma_prefetch_2d(&tmap_v, cb, (int)__ldg(&cs[c + PF].x));
+                if (cp < nchunks) tc::tma_prefetch_2d(&tmap_v, cb, (int)xp);
                 {
                     TPROF_BEGIN;
                     if (c >= NV) tc::mbar_wait_sleep(&sm.v_empty[sv], ((c / NV) - 1) & 1);
                     TPROF_END(0);
                 }
+                sm.Es[sv] = e;
                 if (dbg & 8) {
                     tc::mbar_arrive(&sm.v_full[sv]);
-                    continue;
+                } else {
+                    tc::mbar_arrive_expect_tx(&sm.v_full[sv], (uint32_t)V_STAGE + nk * 16);
+                    tc::tma_load_2d(&sm.Vs[sv][0], &tmap_v, cb, (int)e.x, &sm.v_full[sv]);
+                    tc::bulk_g2s(&sm.Gs[sv][0], pd.geo + e.x, nk * 16, &sm.v_full[sv]);
                 }
-                tc::mbar_arrive_expect_tx(&sm.v_full[sv], (uint32_t)V_STAGE + nk * 16);
-                tc::tma_load_2d(&sm.Vs[sv][0], &tmap_v, cb, (int)e.x, &sm.v_full[sv]);
-                tc::bulk_g2s(&sm.Gs[sv][0], pd.geo + e.x, nk * 16, &sm.v_full[sv]);
             }
+            __syncwarp();
         }
-        __syncwarp();
     } else if (warp >= 4 && warp < 8) {
         // ============================ A producers ============================
         const int q4 = warp & 3;
         const int chl = q4 * 32 + lane;            // channel within the block = TMEM lane
         const bool ch_ok = cb + chl < C && !(dbg & 4);
-        SchedQ sq;
-        sq.init(cs, nchunks);
         int since = 0, prom = 0;
         for (int c = 0; c < nchunks; ++c) {
-            const uint4 e = sq.pop(c);
             if constexpr (PROMOTE) {
                 if (since >= promote_every) {
                     // D -> out slice (this warp's lane quarter, all touched blocks).  The
@@ -505,16 +483,6 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                         uint32_t r[16];
                         tc::tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * TC_N), r);
                         tc::wait_ld();
-                        if (dbg & 512) {     // debug: is D still changing during the promotion?
-                            __nanosleep(5000);
-                            uint32_t r2[16];
-                            tc::tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * TC_N), r2);
-                            tc::wait_ld();
-                            int nd = 0;
-#pragma unroll
-                            for (int n = 0; n < 16; ++n) nd += r2[n] != r[n];
-                            if (nd) atomicAdd(&g_tc_prof[12], (unsigned long long)nd);
-                        }
                         if (ch < C) {
                             const int bi = i0 + (b % TC_BX) * 4, bj = j0 + (b / TC_BX) * 4;
 #pragma unroll
@@ -535,26 +503,28 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const int sv = c % NV, sa = c % NA;
             {
                 TPROF_BEGIN;
-                tc::mbar_wait(&sm.v_full[sv], (c / NV) & 1);
-                TPROF_END(0);
-            }
-            uint32_t hi[TC_KC], lo[TC_KC];
-            const float* vs = reinterpret_cast<const float*>(&sm.Vs[sv][0]) + chl;
-#pragma unroll
-            for (int k = 0; k < TC_KC; ++k) {
-                const float v = ((uint32_t)k < (e.y & 63) && ch_ok) ? vs[k * TC_M] : 0.0f;
-                tc::split_tf32(v, hi[k], lo[k]);
-            }
-            tc::mbar_arrive(&sm.v_empty[sv]);
-            {
-                TPROF_BEGIN;
                 if (c >= NA) tc::mbar_wait_sleep(&sm.a_empty[sa], ((c / NA) - 1) & 1);
                 TPROF_END(1);
             }
+            {
+                TPROF_BEGIN;
+                tc::mbar_wait(&sm.v_full[sv], (c / NV) & 1);
+                TPROF_END(0);
+            }
             tc::fence_after_sync();
+            uint32_t hi[TC_KC], lo[TC_KC];
+            const float* vs = reinterpret_cast<const float*>(&sm.Vs[sv][0]) + chl;
+            const uint32_t nk = sm.Es[sv].y & 63;
+#pragma unroll
+            for (int k = 0; k < TC_KC; ++k) {
+                const float v = ((uint32_t)k < nk && ch_ok) ? vs[k * TC_M] : 0.0f;
+                tc::split_tf32(v, hi[k], lo[k]);
+            }
             const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + A_COL0 + sa * 64;
             tc::tmem_st32(ta, hi);
             tc::tmem_st32(ta + 32, lo);
+            // the tcgen05.st consumed every value loaded from the stage: release it
+            tc::mbar_arrive(&sm.v_empty[sv]);
             tc::wait_st();
             tc::fence_before_sync();
             tc::mbar_arrive(&sm.a_full[sa]);
@@ -570,12 +540,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const int cj = j0 + by * 4 + rr;
             cosr[by] = cj < g.ny ? __ldg(&pd.cos_row[cj]) : 1.0f;
         }
-        SchedQ sq;
-        sq.init(cs, nchunks);
         for (int c = 0; c < nchunks; ++c) {
-            const uint4 e = sq.pop(c);
-            const uint32_t pstart = e.x, nk = e.y & 63, mask = e.z, blist = e.w;
-            const int row = (int)(e.y >> 6);
             const int sv = c % NV;
             float4 g4[4];
             {
@@ -583,20 +548,19 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 tc::mbar_wait(&sm.v_full[sv], (c / NV) & 1);
                 TPROF_END(2);
             }
+            const uint4 e = sm.Es[sv];
+            const uint32_t pstart = e.x, nk = e.y & 63, mask = e.z, blist = e.w;
+            const int row = (int)(e.y >> 6);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 g4[u] = sm.Gs[sv][4 * kq + u];
                 if ((uint32_t)(4 * kq + u) >= nk) g4[u] = make_float4(0.0f, kInvalidDy, 0.0f, 0.0f);
             }
-            tc::mbar_arrive(&sm.v_empty[sv]);
+
             const int sb = c % NBS;
             {
                 TPROF_BEGIN;
                 if (c >= NBS) tc::mbar_wait(&sm.b_empty[sb], ((c / NBS) - 1) & 1);
-                if ((dbg & 2048) && c >= 2) {   // debug: at most 2 chunks ahead of the issuer
-                    const int c2 = c - 2;
-                    tc::mbar_wait(&sm.b_empty[c2 % NBS], (c2 / NBS) & 1);
-                }
                 TPROF_END(0);
             }
             TPROF_BEGIN;
@@ -641,8 +605,14 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     *reinterpret_cast<uint4*>(bst + B_HALF + o) = l4;
                 }
             }
+            if (wt == 0) sm.Bmask[sb] = mask;
             if (!(dbg & 128)) tc::fence_proxy_async_smem();
             tc::mbar_arrive(&sm.b_full[sb]);
+            // release the V stage only now: an mbarrier arrive does not wait for this
+            // thread's outstanding shared-memory loads (the SASS arrive carries no
+            // scoreboard wait), so the stage (Es, Gs) is handed back after every value
+            // read from it has been consumed
+            tc::mbar_arrive(&sm.v_empty[sv]);
             TPROF_END(1);
         }
     }
@@ -781,7 +751,7 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
                 "epilogue %.2f (fractions of CTA time)\n",
                 grid.x * grid.y, tot / (grid.x * grid.y), h[1] / tot, h[2] / tot, h[10] / tot,
                 h[3] / tot, h[4] / tot, h[5] / tot, h[11] / tot, h[7] / tot, h[6] / tot, h[9] / tot);
-        fprintf(stderr, "[tc prof] D changed during promotion reads: %llu\n", h[12]);
+        fprintf(stderr, "[tc prof] debug counter: %llu\n", h[12]);
         unsigned long long z[16] = {0};
         cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
     }

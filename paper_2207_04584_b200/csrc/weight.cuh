@@ -31,7 +31,12 @@ __device__ __forceinline__ double wrap180_d(double x) {
 }
 
 // fp64 support test d <= R for cell (i, j) and a sample at (lon_s, lat_s) degrees.
-static __device__ __noinline__ bool support_fp64(const Geom& g, int i, int j, double lon_s,
+#ifdef HG_SUPPORT_INLINE
+static __device__ __forceinline__
+#else
+static __device__ __noinline__
+#endif
+bool support_fp64(const Geom& g, int i, int j, double lon_s,
                                           double lat_s) {
     double lon_c = __dadd_rn(g.crval_lon,
                              __dmul_rn(__dadd_rn(__dadd_rn((double)i, 1.0), -g.crpix_x),
@@ -99,7 +104,7 @@ __device__ __forceinline__ void patch4x4_weights(const Geom& g, const PlanDev& p
     const float hlon = 0.5f * g.dlon_rad, hlat = 0.5f * g.dlat_rad;
     const float fy = (float)(br - g.mlat - cj);
     const int ix = -g.mlon - ci0;
-    bool band = false;
+    uint32_t band = 0;      // bit 4u + cc: pair inside the guard band
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const float a = fminf(fabsf((fy + s[u].y) * hlat), 1.0f);
@@ -115,30 +120,27 @@ __device__ __forceinline__ void patch4x4_weights(const Geom& g, const PlanDev& p
             const float h = fmaf(ccs, sbv, sa);
             // 4 asin^2(sqrt h) = h (4 + 4h/3 + 32h^2/45 + ...)
             const float d2 = h * fmaf(h, fmaf(h, 32.0f / 45.0f, 4.0f / 3.0f), 4.0f);
-            band |= (d2 > g.R2_lo) & (d2 <= g.R2_hi);
+            band |= (uint32_t)((d2 > g.R2_lo) & (d2 <= g.R2_hi)) << (4 * u + cc);
             const float e = ex2_approx(d2 * g.neg_k2);
-            w[u][cc] = d2 <= g.R2_lo ? e : 0.0f;
+            w[u][cc] = d2 <= g.R2_hi ? e : 0.0f;     // band pairs provisionally in
         }
     }
-    if (band) {   // rare: decide the guard band in fp64 (recomputes the flagged pairs)
+#ifdef HG_W_NORECHECK
+    band = 0;
+#endif
+    if (band) {   // rare: decide the guard-band pairs in fp64 (one call site, no array indexing)
+        uint32_t kill = 0;
 #pragma unroll 1
-        for (int k = 0; k < 16; ++k) {
-            const int u = k >> 2, cc = k & 3;
-            const float a = fminf(fabsf((fy + s[u].y) * hlat), 1.0f);
-            const float a2 = a * a;
-            const float sa = fmaf(a2 * (-1.0f / 3.0f), a2, a2);
-            const float ccs = cos_c * s[u].z;
-            const float b0 = ((float)(__float_as_int(s[u].w) + ix) + s[u].x) * hlon;
-            const float bb = b0 - (float)cc * hlon;
-            const float b2 = bb * bb;
-            const float sbv = fmaf(b2 * (-1.0f / 3.0f), b2, b2);
-            const float h = fmaf(ccs, sbv, sa);
-            const float d2 = h * fmaf(h, fmaf(h, 32.0f / 45.0f, 4.0f / 3.0f), 4.0f);
-            if (d2 > g.R2_lo && d2 <= g.R2_hi && ci0 + cc < g.nx) {
+        for (uint32_t m = band; m; m &= m - 1) {
+            const int k = __ffs(m) - 1, u = k >> 2, cc = k & 3;
+            if (ci0 + cc < g.nx) {
                 const double2 ll = pd.ll[p0 + u];
-                w[u][cc] = support_fp64(g, ci0 + cc, cj, ll.x, ll.y) ? ex2_approx(d2 * g.neg_k2) : 0.0f;
+                if (!support_fp64(g, ci0 + cc, cj, ll.x, ll.y)) kill |= 1u << k;
             }
         }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if ((kill >> k) & 1u) w[k >> 2][k & 3] = 0.0f;
     }
     if (ci0 + 4 > g.nx) {
 #pragma unroll
