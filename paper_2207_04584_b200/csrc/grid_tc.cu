@@ -73,10 +73,13 @@ constexpr int NV = HG_TC_NV;              // V staging stages (SMEM)
 constexpr int MAXQ = 8;                   // max blocks (B slots) per chunk entry
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t A_COL0 = TC_NB * TC_N; // 256: A stages after the accumulators
-// B stage layout (per hi / lo half): [k-step 4][k-core 2][row group 2*MAXQ slots][8 rows][16 B]
-constexpr uint32_t B_LBO = 2 * MAXQ * 128;           // 2048: between the 2 K core matrices
-constexpr uint32_t B_KS = 2 * B_LBO;                 // 4096: between K-steps
-constexpr uint32_t B_HALF = (TC_KC / 8) * B_KS;      // 16 KB
+// B stage layout (per hi / lo half): K-major, 128-byte swizzle.  Row R = 16 q + n (slot q,
+// cell n) holds the chunk's 32 tf32 weights (128 B); 8-row groups are 1024-B swizzle atoms
+// (SBO = 1024); the 16-B k-quad j of row R sits at chunk position j ^ (R & 7), so the 32
+// lanes of a producer warp storing one k-quad each hit 8 distinct bank groups (no
+// conflicts); the MMA K-step ks starts 32 B further into the atom.
+constexpr uint32_t B_ROW = TC_KC * 4;                // 128 B
+constexpr uint32_t B_HALF = MAXQ * TC_N * B_ROW;     // 16 KB
 constexpr uint32_t B_STAGE = 2 * B_HALF;             // 32 KB (hi + lo)
 constexpr int V_ROW = TC_M * 4;                      // 512 B
 constexpr int V_STAGE = TC_KC * V_ROW;               // 16 KB
@@ -95,9 +98,9 @@ struct TcSmem {
 };
 
 // byte offset of (slot q, cell n, sample k) inside one half (hi or lo) of a B stage
-__device__ __forceinline__ uint32_t b_off(int q, int n, int k) {
-    return (uint32_t)((k >> 3) * B_KS + ((k >> 2) & 1) * B_LBO + (2 * q + (n >> 3)) * 128 +
-                      (n & 7) * 16);
+__device__ __forceinline__ uint32_t b_off(int q, int n, int kq) {
+    const int r = q * TC_N + n;
+    return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((kq ^ (r & 7)) << 4));
 }
 
 // ------------------------------------------------------------------ plan-side pieces
@@ -298,6 +301,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
            float* __restrict__ wout, int promote_every, int dbg) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_raw);
+    if (tc::smem_u32(smem_raw) & 1023u) __trap();   // swizzle atoms need 1024-B alignment
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool prof = (dbg & 32) != 0;
     const long long t_start = clock64();
@@ -389,7 +393,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             if (!(dbg & 2)) {
                 // whole warp walks the runs (uniform values); each run is one 12-MMA block
                 // behind a single elect; descriptors advance by (byte offset >> 4)
-                const uint64_t dh0 = tc::sdesc(tc::smem_u32(&sm.B[sb][0]), B_LBO, 128);
+                const uint64_t dh0 = tc::sdesc_sw128(tc::smem_u32(&sm.B[sb][0]));
                 const uint32_t a0 = tmem + A_COL0 + sa * 64;
                 uint32_t mm = mask;
                 int q = 0;
@@ -400,8 +404,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     const uint32_t same = mm & (tb ? touched : ~touched);
                     const int r = __ffs(~(same >> b)) - 1;
                     mm &= ~(((1u << r) - 1u) << b);
-                    tc::mma_run_3xtf32<(B_KS >> 4), (B_HALF >> 4)>(
-                        tmem + (uint32_t)(b * TC_N), a0, dh0 + (uint64_t)((2 * q * 128) >> 4),
+                    tc::mma_run_3xtf32<(32 >> 4), (B_HALF >> 4)>(
+                        tmem + (uint32_t)(b * TC_N), a0, dh0 + (uint64_t)((q * TC_N * B_ROW) >> 4),
                         tc::idesc_tf32(TC_M, TC_N * r), tb);
                     touched |= ((1u << r) - 1u) << b;
                     q += r;
@@ -600,7 +604,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     tc::split_tf32(w[1][cc], h4.y, l4.y);
                     tc::split_tf32(w[2][cc], h4.z, l4.z);
                     tc::split_tf32(w[3][cc], h4.w, l4.w);
-                    const uint32_t o = b_off(q, n, kq * 4);
+                    const uint32_t o = b_off(q, n, kq);
                     *reinterpret_cast<uint4*>(bst + o) = h4;
                     *reinterpret_cast<uint4*>(bst + B_HALF + o) = l4;
                 }

@@ -198,6 +198,19 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
     return d;                                 // base offset 0, layout SWIZZLE_NONE (0)
 }
 
+// Shared-memory matrix descriptor, K-major with 128-byte swizzle: 8-row x 128-B atoms
+// (1024-B aligned), SBO = 1024 B between 8-row groups, LBO unused (1).  Advancing along K
+// inside the atom adds the byte offset (>> 4) to the start address.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                   // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;         // SBO
+    d |= (uint64_t)1 << 46;                   // version (sm_100)
+    d |= (uint64_t)2 << 61;                   // layout: SWIZZLE_128B
+    return d;
+}
+
 // ---- TMEM <-> registers (32 lanes x 32 bit, per warp) ------------------------------
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
