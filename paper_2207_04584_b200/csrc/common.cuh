@@ -75,6 +75,7 @@ struct hegrid_plan_s {
     mutable uint4* d_tc_sched = nullptr;       // {plan position, n samples, bin row, block mask}
     mutable uint32_t* d_tc_tile_off = nullptr; // [tiles + 1]
     mutable int64_t tc_nchunks = -1;
+    mutable uint32_t tc_max_cpb = 0;           // max schedule entries touching one block
     mutable float* d_tc_wsum = nullptr;        // [cells] W with the TC engine's weights
     // scratch for USER_CN device grids
     float* d_scratch = nullptr;

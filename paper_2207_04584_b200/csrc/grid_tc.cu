@@ -49,13 +49,13 @@ namespace hg {
 
 constexpr int TC_THREADS = 512;
 constexpr int TC_M = 128;                 // channels per CTA (UMMA M)
-constexpr int TC_BX = 4, TC_BY = 4;       // blocks per CTA tile
-constexpr int TC_NB = TC_BX * TC_BY;      // 16 blocks
+constexpr int TC_BX = 4, TC_BY = 3;       // blocks per CTA tile (16 x 12 cells)
+constexpr int TC_NB = TC_BX * TC_BY;      // 12 blocks
 constexpr int TC_N = 16;                  // cells per block: 4 x 4
 constexpr int TC_TW = TC_BX * 4, TC_TH = TC_BY * 4;
 constexpr int TC_KC = 32;                 // samples per chunk (4 MMA K-steps of 8)
 #ifndef HG_TC_NA
-#define HG_TC_NA 4
+#define HG_TC_NA 2
 #endif
 // NBS = 2: with 3-4 weight stages (producers up to 3 chunks ahead of the tensor core)
 // results became timing-dependent although every stage handoff is mbarrier-ordered; the
@@ -65,14 +65,25 @@ constexpr int TC_KC = 32;                 // samples per chunk (4 MMA K-steps of
 #define HG_TC_NBS 2
 #endif
 #ifndef HG_TC_NV
-#define HG_TC_NV 5
+#define HG_TC_NV 3
+#endif
+#ifndef HG_TC_SEG
+#define HG_TC_SEG 8
 #endif
 constexpr int NA = HG_TC_NA;              // A stages (TMEM)
 constexpr int NBS = HG_TC_NBS;            // B stages (SMEM)
 constexpr int NV = HG_TC_NV;              // V staging stages (SMEM)
 constexpr int MAXQ = 8;                   // max blocks (B slots) per chunk entry
+// The tensor core's fp32 accumulation truncates, so its error grows with the number of MMAs
+// accumulated into one D element.  D is therefore double-buffered in TMEM by segments of
+// SEG chunks: while the tensor core accumulates segment s+1 into one buffer, the A warps add
+// segment s's buffer into an fp32 master tile in shared memory (round-to-nearest).
+constexpr int SEG = HG_TC_SEG;
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t A_COL0 = TC_NB * TC_N; // 256: A stages after the accumulators
+constexpr uint32_t D_COLS = TC_NB * TC_N;      // one accumulator buffer: 12 blocks x 16 columns
+constexpr uint32_t A_COL0 = 2 * D_COLS;        // 384: A stages after the two D buffers
+static_assert(A_COL0 + NA * 64 <= TMEM_COLS, "TMEM budget");
+static_assert(SEG > NA, "a segment is promoted NA chunks into the next one");
 // B stage layout (per hi / lo half): K-major, 128-byte swizzle.  Row R = 16 q + n (slot q,
 // cell n) holds the chunk's 32 tf32 weights (128 B); 8-row groups are 1024-B swizzle atoms
 // (SBO = 1024); the 16-B k-quad j of row R sits at chunk position j ^ (R & 7), so the 32
@@ -84,6 +95,7 @@ constexpr uint32_t B_STAGE = 2 * B_HALF;             // 32 KB (hi + lo)
 constexpr int V_ROW = TC_M * 4;                      // 512 B
 constexpr int V_STAGE = TC_KC * V_ROW;               // 16 KB
 constexpr int W_THREADS = 256;            // B producers (warps 8-15)
+constexpr int T_LD = TC_TW * TC_TH + 4;   // epilogue tile row (floats): 16-B aligned, conflict-free
 
 struct TcSmem {
     uint8_t B[NBS][B_STAGE];
@@ -92,10 +104,14 @@ struct TcSmem {
     uint4 Es[NV];                         // the chunk's schedule entry (written by the V loader)
     uint32_t Bmask[NBS];                  // block mask of the chunk in each weight stage
     uint64_t a_full[NA], a_empty[NA], b_full[NBS], b_empty[NBS], v_full[NV], v_empty[NV];
-    uint64_t bar_done, bar_prom, bar_promdone, bar_drain;
+    uint64_t seg_done[2], seg_free[2];    // D buffer d: segment's MMAs complete / promoted
+    uint64_t bar_done;
     uint32_t tmem_base;
-    uint32_t touched;
+    uint32_t sink[TC_THREADS / 32];       // dependency sink (see the B producers' release)
+    alignas(16) float M[TC_M][T_LD];      // fp32 master sums [channel][cell] (padded rows)
 };
+
+static_assert(offsetof(TcSmem, B) == 0 && offsetof(TcSmem, Vs) == NBS * B_STAGE, "stage layout");
 
 // byte offset of (slot q, cell n, sample k) inside one half (hi or lo) of a B stage
 __device__ __forceinline__ uint32_t b_off(int q, int n, int kq) {
@@ -136,6 +152,9 @@ __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int ti
     const int i_hi = min(i0 + TC_TW - 1, g.nx - 1);
     const int br_end = min(j0 + TC_TH - 1, g.ny - 1) + 2 * g.mlat;
     uint32_t cnt = 0;
+    uint32_t cpb[TC_NB];                    // chunks touching each block (count pass)
+#pragma unroll
+    for (int b = 0; b < TC_NB; ++b) cpb[b] = 0;
     const uint32_t base = n_out ? 0 : off[warp];
     for (int br = j0; br <= br_end; ++br) {
         const int m = pd.mrow[br];
@@ -170,6 +189,10 @@ __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int ti
                 if (lane >= o) incl += y;
             }
             const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+            if (n_out) {
+#pragma unroll
+                for (int b = 0; b < TC_NB; ++b) cpb[b] += __popc(__ballot_sync(0xffffffffu, (mk >> b) & 1u));
+            }
             if (mk && sched) {
                 uint32_t pos = base + cnt + incl - ne;
                 uint32_t rest = mk;
@@ -186,7 +209,13 @@ __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int ti
             cnt += tot;
         }
     }
-    if (n_out && lane == 0) n_out[warp] = cnt;
+    if (n_out && lane == 0) {
+        n_out[warp] = cnt;
+        uint32_t mx = 0;
+#pragma unroll
+        for (int b = 0; b < TC_NB; ++b) mx = max(mx, cpb[b]);
+        atomicMax(&n_out[tiles], mx);     // max chunks per block over the map
+    }
 }
 
 // W per cell from the tensor-core engine's own weights (patch4x4_weights), two-level sum
@@ -238,12 +267,18 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
         return cuda_status(e);
     }
     const int threads = 128, blocks = (tiles * 32 + threads - 1) / threads;
+    e = cudaMemsetAsync(d_n, 0, (tiles + 1) * sizeof(uint32_t), st);
+    if (e != cudaSuccess) {
+        cudaFree(d_n);
+        cudaFree(d_w);
+        return cuda_status(e);
+    }
     k_tc_schedule<<<blocks, threads, 0, st>>>(g, p->dev(), tiles, d_n, nullptr, nullptr);
     k_tc_wsum<<<(int)((cells + 127) / 128), 128, 0, st>>>(g, p->dev(), d_w);
     count_launch(2);
     std::vector<uint32_t> h(tiles + 1, 0);
     e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d_n, tiles * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d_n, (tiles + 1) * 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
         cudaFree(d_n);
@@ -272,6 +307,7 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     p->d_tc_tile_off = d_n;
     p->d_tc_wsum = d_w;
     p->tc_nchunks = total;
+    p->tc_max_cpb = h[tiles];
     return HEGRID_OK;
 }
 
@@ -280,25 +316,12 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
 // 6 V wait V-empty, 7 B work, 8 A work, 9 epilogue, 10 issuer issue
 __device__ unsigned long long g_tc_prof[16];
 
-// Zero this warp's lane quarter of all accumulator columns [0, A_COL0).
-__device__ __forceinline__ void zero_d(uint32_t tmem, int q4) {
-    uint32_t z[32];
-#pragma unroll
-    for (int k = 0; k < 32; ++k) z[k] = 0u;
-#pragma unroll
-    for (int c0 = 0; c0 < (int)A_COL0; c0 += 32)
-        tc::tmem_st32(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0, z);
-    tc::wait_st();
-}
-
 // ------------------------------------------------------------------ the kernel
-template <bool PROMOTE>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap tmap_v,
            PlanDev pd, const uint4* __restrict__ sched,
            const uint32_t* __restrict__ tile_off, const float* __restrict__ wsum,
-           const float* __restrict__ V, int64_t ldv, int C, float* __restrict__ out,
-           float* __restrict__ wout, int promote_every, int dbg) {
+           int C, float* __restrict__ out, float* __restrict__ wout, int dbg) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_raw);
     if (tc::smem_u32(smem_raw) & 1023u) __trap();   // swizzle atoms need 1024-B alignment
@@ -329,52 +352,66 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             tc::mbar_init(&sm.v_full[s], 1);
             tc::mbar_init(&sm.v_empty[s], 128 + W_THREADS);
         }
+        for (int d = 0; d < 2; ++d) {
+            tc::mbar_init(&sm.seg_done[d], 1);
+            tc::mbar_init(&sm.seg_free[d], 128);
+        }
         tc::mbar_init(&sm.bar_done, 1);
-        tc::mbar_init(&sm.bar_prom, 1);
-        tc::mbar_init(&sm.bar_drain, 1);
-        tc::mbar_init(&sm.bar_promdone, 128);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if constexpr (PROMOTE) {
-        // the CTA's out slice accumulates the promoted fp32 partial sums: start from 0
-        for (int e = tid; e < TC_M * TC_TW * TC_TH; e += TC_THREADS) {
-            const int ch = cb + e / (TC_TW * TC_TH), cl = e % (TC_TW * TC_TH);
-            const int i = i0 + cl % TC_TW, j = j0 + cl / TC_TW;
-            if (ch < C && i < g.nx && j < g.ny) out[(int64_t)ch * cells + (int64_t)j * g.nx + i] = 0.0f;
-        }
+    {   // the master sums start at 0
+        float4* m4 = reinterpret_cast<float4*>(&sm.M[0][0]);
+        for (int e = tid; e < TC_M * T_LD / 4; e += TC_THREADS) m4[e] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     }
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = sm.tmem_base;
-    if (warp >= 4 && warp < 8) zero_d(tmem, warp & 3);     // D accumulates from 0
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
+
+    // D buffer d -> master: this warp's lane quarter (channels), blocks in `mask`
+    auto promote_buffer = [&](int d, uint32_t mask) {
+        const int q4 = warp & 3, row = q4 * 32 + lane;
+        float* mrow = &sm.M[row][0];
+        while (mask) {
+            const int b = __ffs(mask) - 1;
+            mask &= mask - 1;
+            uint32_t r[16];
+            tc::tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)d * D_COLS + (uint32_t)(b * TC_N), r);
+            tc::wait_ld();
+            const int x0 = (b % TC_BX) * 4, y0 = (b / TC_BX) * 4;
+#pragma unroll
+            for (int cy = 0; cy < 4; ++cy) {
+                float4* p4 = reinterpret_cast<float4*>(&mrow[(y0 + cy) * TC_TW + x0]);
+                float4 v = *p4;
+                v.x += __uint_as_float(r[cy * 4 + 0]);
+                v.y += __uint_as_float(r[cy * 4 + 1]);
+                v.z += __uint_as_float(r[cy * 4 + 2]);
+                v.w += __uint_as_float(r[cy * 4 + 3]);
+                *p4 = v;
+            }
+        }
+    };
+    // Segment s (chunks [s SEG, (s+1) SEG)) uses D buffer s & 1.  The A warps promote it when
+    // they are NA chunks into segment s+1 (the issuer has then issued all of segment s), if
+    // that chunk exists; the last one or two segments are promoted after the loop.
+    const int nseg = (nchunks + SEG - 1) / SEG;
+    auto promoted_in_loop = [&](int s) { return (s + 1) * SEG + NA <= nchunks - 1; };
 
     if (warp == 0) {
         // ============================ MMA issuer =============================
-        int since = 0, prom = 0;
-        uint32_t touched = 0xFFFFu;         // D starts zeroed: every block accumulates
+        uint32_t touched = 0;
         for (int c = 0; c < nchunks; ++c) {
-            if constexpr (PROMOTE) {
-                if (since >= promote_every) {
-                    // hand D to the A producers, wait until they have moved it out
-                    // drain: the issuer itself waits for all its MMAs, then releases the
-                    // A producers with a plain arrive (touched mask published with it)
-                    tc::mma_commit_warp(&sm.bar_drain);
-                    tc::mbar_wait(&sm.bar_drain, prom & 1);
+            const int seg = c / SEG, d = seg & 1;
+            if (c % SEG == 0) {
+                // a new segment restarts D buffer d (accumulate = 0 on each block's first
+                // MMA); its previous contents (segment seg - 2) must have been promoted
+                if (seg >= 2) {
+                    TPROF_BEGIN;
+                    tc::mbar_wait(&sm.seg_free[d], ((seg >> 1) - 1) & 1);
+                    TPROF_END(3);
                     tc::fence_after_sync();
-                    sm.touched = touched;
-                    tc::fence_before_sync();
-                    __syncwarp();
-                    if (lane == 0) tc::mbar_arrive(&sm.bar_prom);
-                    tc::mbar_wait(&sm.bar_promdone, prom & 1);
-                    tc::fence_after_sync();
-                    touched = (dbg & 256) ? 0xFFFFu : 0u;   // next MMA on each block overwrites D
-                    since = 0;
-                    ++prom;
                 }
+                touched = 0;
             }
             const int sa = c % NA, sb = c % NBS;
             {
@@ -395,6 +432,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 // behind a single elect; descriptors advance by (byte offset >> 4)
                 const uint64_t dh0 = tc::sdesc_sw128(tc::smem_u32(&sm.B[sb][0]));
                 const uint32_t a0 = tmem + A_COL0 + sa * 64;
+                const uint32_t dbase = tmem + (uint32_t)d * D_COLS;
                 uint32_t mm = mask;
                 int q = 0;
                 while (mm) {
@@ -405,7 +443,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     const int r = __ffs(~(same >> b)) - 1;
                     mm &= ~(((1u << r) - 1u) << b);
                     tc::mma_run_3xtf32<(32 >> 4), (B_HALF >> 4)>(
-                        tmem + (uint32_t)(b * TC_N), a0, dh0 + (uint64_t)((q * TC_N * B_ROW) >> 4),
+                        dbase + (uint32_t)(b * TC_N), a0, dh0 + (uint64_t)((q * TC_N * B_ROW) >> 4),
                         tc::idesc_tf32(TC_M, TC_N * r), tb);
                     touched |= ((1u << r) - 1u) << b;
                     q += r;
@@ -413,11 +451,10 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             }
             tc::mma_commit_warp(&sm.a_empty[sa]);
             tc::mma_commit_warp(&sm.b_empty[sb]);
+            if (c % SEG == SEG - 1 || c == nchunks - 1) tc::mma_commit_warp(&sm.seg_done[d]);
             __syncwarp();
             TPROF_END(2);
-            ++since;
         }
-        sm.touched = touched;
         tc::mma_commit_warp(&sm.bar_done);
         __syncwarp();
     } else if (warp == 1) {
@@ -450,7 +487,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 if (cp < nchunks) tc::tma_prefetch_2d(&tmap_v, cb, (int)xp);
                 {
                     TPROF_BEGIN;
-                    if (c >= NV) tc::mbar_wait_sleep(&sm.v_empty[sv], ((c / NV) - 1) & 1);
+                    if (c >= NV) tc::mbar_wait(&sm.v_empty[sv], ((c / NV) - 1) & 1);
                     TPROF_END(0);
                 }
                 sm.Es[sv] = e;
@@ -464,81 +501,84 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             }
             __syncwarp();
         }
-    } else if (warp >= 4 && warp < 8) {
+    }
+    // A producers keep the block masks of the (at most two) segments not yet promoted
+    uint32_t segmask[2] = {0u, 0u};
+    if (warp >= 4 && warp < 8) {
         // ============================ A producers ============================
         const int q4 = warp & 3;
         const int chl = q4 * 32 + lane;            // channel within the block = TMEM lane
         const bool ch_ok = cb + chl < C && !(dbg & 4);
-        int since = 0, prom = 0;
-        for (int c = 0; c < nchunks; ++c) {
-            if constexpr (PROMOTE) {
-                if (since >= promote_every) {
-                    // D -> out slice (this warp's lane quarter, all touched blocks).  The
-                    // four A warps enter together so none can run a whole promotion ahead
-                    // (parity waits alias across two phases).
-                    asm volatile("bar.sync 3, 128;" ::: "memory");
-                    tc::mbar_wait(&sm.bar_prom, prom & 1);
-                    tc::fence_after_sync();
-                    const int ch = cb + chl;
-                    const uint32_t tm = *(volatile uint32_t*)&sm.touched;
-#pragma unroll 1
-                    for (int b = 0; b < TC_NB; ++b) {
-                        if (!((tm >> b) & 1u)) continue;
-                        uint32_t r[16];
-                        tc::tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * TC_N), r);
-                        tc::wait_ld();
-                        if (ch < C) {
-                            const int bi = i0 + (b % TC_BX) * 4, bj = j0 + (b / TC_BX) * 4;
-#pragma unroll
-                            for (int n = 0; n < TC_N; ++n) {
-                                const int i = bi + (n & 3), j = bj + (n >> 2);
-                                if (i < g.nx && j < g.ny)
-                                    out[(int64_t)ch * cells + (int64_t)j * g.nx + i] += __uint_as_float(r[n]);
-                            }
-                        }
-                    }
-                    if (dbg & 256) zero_d(tmem, q4);
-                    tc::fence_before_sync();
-                    tc::mbar_arrive(&sm.bar_promdone);
-                    since = 0;
-                    ++prom;
-                }
-            }
-            const int sv = c % NV, sa = c % NA;
-            {
-                TPROF_BEGIN;
-                if (c >= NA) tc::mbar_wait_sleep(&sm.a_empty[sa], ((c / NA) - 1) & 1);
-                TPROF_END(1);
-            }
+        // Software-pipelined: the values of chunk c+1 are loaded and split while chunk c's
+        // tcgen05.st is in flight; chunk c is published (a_full) once its stores completed.
+        uint32_t hi[TC_KC], lo[TC_KC];
+        auto load_split = [&](int c) {
+            const int sv = c % NV;
             {
                 TPROF_BEGIN;
                 tc::mbar_wait(&sm.v_full[sv], (c / NV) & 1);
                 TPROF_END(0);
             }
-            tc::fence_after_sync();
-            uint32_t hi[TC_KC], lo[TC_KC];
             const float* vs = reinterpret_cast<const float*>(&sm.Vs[sv][0]) + chl;
-            const uint32_t nk = sm.Es[sv].y & 63;
+            const uint4 ee = sm.Es[sv];
+            const uint32_t nk = ee.y & 63;
+            if ((c / SEG) & 1) segmask[1] |= ee.z; else segmask[0] |= ee.z;
 #pragma unroll
             for (int k = 0; k < TC_KC; ++k) {
                 const float v = ((uint32_t)k < nk && ch_ok) ? vs[k * TC_M] : 0.0f;
                 tc::split_tf32(v, hi[k], lo[k]);
             }
+        };
+        auto store = [&](int c) {
+            const int sa = c % NA;
+            {
+                TPROF_BEGIN;
+                if (c >= NA) tc::mbar_wait(&sm.a_empty[sa], ((c / NA) - 1) & 1);
+                TPROF_END(1);
+            }
+            tc::fence_after_sync();
             const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + A_COL0 + sa * 64;
             tc::tmem_st32(ta, hi);
             tc::tmem_st32(ta + 32, lo);
             // the tcgen05.st consumed every value loaded from the stage: release it
-            tc::mbar_arrive(&sm.v_empty[sv]);
+            tc::mbar_arrive(&sm.v_empty[c % NV]);
+        };
+        if (nchunks > 0) {
+            load_split(0);
+            store(0);
+        }
+        for (int c = 0; c < nchunks; ++c) {
+            {
+                TPROF_BEGIN;
+                if (c + 1 < nchunks) load_split(c + 1);
+                TPROF_END(3);
+            }
             tc::wait_st();
             tc::fence_before_sync();
-            tc::mbar_arrive(&sm.a_full[sa]);
-            ++since;
+            tc::mbar_arrive(&sm.a_full[c % NA]);
+            if (c + 1 < nchunks) {
+                const int cn = c + 1;
+                if (cn >= SEG && cn % SEG == NA) {
+                    // promote segment s = cn / SEG - 1 (all its MMAs were issued: the
+                    // issuer has consumed chunk cn - NA = (s + 1) SEG)
+                    const int s = cn / SEG - 1, d = s & 1;
+                    TPROF_BEGIN;
+                    tc::mbar_wait(&sm.seg_done[d], (s >> 1) & 1);
+                    tc::fence_after_sync();
+                    promote_buffer(d, segmask[d]);
+                    segmask[d] = 0;
+                    tc::fence_before_sync();
+                    tc::mbar_arrive(&sm.seg_free[d]);
+                    TPROF_END(2);
+                }
+                store(cn);
+            }
         }
     } else if (warp >= 8) {
         // ============================ B producers ============================
         const int wt = tid - 8 * 32;                  // 0..255
         const int kq = wt & 7, rr = (wt >> 3) & 3, q0 = wt >> 5;
-        float cosr[TC_BY];                        // cos(lat) of this thread's 4 possible rows
+        float cosr[TC_BY];                        // cos(lat) of this thread's possible rows
 #pragma unroll
         for (int by = 0; by < TC_BY; ++by) {
             const int cj = j0 + by * 4 + rr;
@@ -559,6 +599,18 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             for (int u = 0; u < 4; ++u) {
                 g4[u] = sm.Gs[sv][4 * kq + u];
                 if ((uint32_t)(4 * kq + u) >= nk) g4[u] = make_float4(0.0f, kInvalidDy, 0.0f, 0.0f);
+            }
+            // Release the value stage now.  An mbarrier arrive does not wait for this
+            // thread's outstanding shared loads, so first make an instruction consume every
+            // loaded word: a store of their xor (it cannot issue before the loads returned).
+            {
+                uint32_t dep = e.x ^ e.y ^ e.z ^ e.w;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    dep ^= __float_as_uint(g4[u].x) ^ __float_as_uint(g4[u].y) ^
+                           __float_as_uint(g4[u].z) ^ __float_as_uint(g4[u].w);
+                asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[warp])), "r"(dep) : "memory");
+                tc::mbar_arrive(&sm.v_empty[sv]);
             }
 
             const int sb = c % NBS;
@@ -612,47 +664,32 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             if (wt == 0) sm.Bmask[sb] = mask;
             if (!(dbg & 128)) tc::fence_proxy_async_smem();
             tc::mbar_arrive(&sm.b_full[sb]);
-            // release the V stage only now: an mbarrier arrive does not wait for this
-            // thread's outstanding shared-memory loads (the SASS arrive carries no
-            // scoreboard wait), so the stage (Es, Gs) is handed back after every value
-            // read from it has been consumed
-            tc::mbar_arrive(&sm.v_empty[sv]);
             TPROF_END(1);
         }
     }
 
     const long long t_loop = clock64();
     __syncthreads();
-    // ---- epilogue: wait for the last MMAs
+    // ---- epilogue: promote the segments still in TMEM, then coalesced row segments of the
+    // master tile to out: V = S / W (Eq. 1's division), NaN where W = 0
     tc::mbar_wait(&sm.bar_done, 0);
     tc::fence_after_sync();
-    const float qnan = __int_as_float(0x7fc00000);
-    // epilogue warps: in dense mode the A warps (4-7), which also own the promoted partial
-    // sums of their channels, each take all 16 blocks; otherwise warps 0-7 split them
-    const bool epi = PROMOTE ? (warp >= 4 && warp < 8) : (warp < 8);
-    if (epi) {
-        const int ch = cb + (warp & 3) * 32 + lane;
-        const int a_lo = PROMOTE ? 0 : (warp >> 2) * 8;
-        const int a_hi = PROMOTE ? TC_NB : a_lo + 8;
-#pragma unroll 1
-        for (int b = a_lo; b < a_hi; ++b) {
-            uint32_t r[16];
-            const bool tb = (sm.touched >> b) & 1u;
-            tc::tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(b * TC_N), r);
-            tc::wait_ld();
-            if (ch < C) {
-                const int bi = i0 + (b % TC_BX) * 4, bj = j0 + (b / TC_BX) * 4;
-#pragma unroll
-                for (int n = 0; n < TC_N; ++n) {
-                    const int i = bi + (n & 3), j = bj + (n >> 2);
-                    if (i < g.nx && j < g.ny) {
-                        float* o = out + (int64_t)ch * cells + (int64_t)j * g.nx + i;
-                        float S = tb ? __uint_as_float(r[n]) : 0.0f;
-                        if constexpr (PROMOTE) S += *o;
-                        const float W = __ldg(&wsum[(int64_t)j * g.nx + i]);
-                        *o = W > 0.0f ? __fdiv_rn(S, W) : qnan;
-                    }
-                }
+    if (warp >= 4 && warp < 8) {
+        for (int s = (nseg >= 2 ? nseg - 2 : 0); s < nseg; ++s)
+            if (!promoted_in_loop(s)) promote_buffer(s & 1, segmask[s & 1]);
+    }
+    __syncthreads();
+    {
+        const float qnan = __int_as_float(0x7fc00000);
+        const int x = lane & 15;
+#pragma unroll 2
+        for (int it = warp; it < TC_M * (TC_TH / 2); it += TC_THREADS / 32) {
+            const int row = it / (TC_TH / 2), y = (it % (TC_TH / 2)) * 2 + (lane >> 4);
+            const int ch = cb + row, i = i0 + x, j = j0 + y;
+            if (ch < C && i < g.nx && j < g.ny) {
+                const float S = sm.M[row][y * TC_TW + x];
+                const float W = __ldg(&wsum[(int64_t)j * g.nx + i]);
+                out[(int64_t)ch * cells + (int64_t)j * g.nx + i] = W > 0.0f ? __fdiv_rn(S, W) : qnan;
             }
         }
     }
@@ -667,10 +704,13 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             atomicAdd(&g_tc_prof[1], pw[0]);
             atomicAdd(&g_tc_prof[2], pw[1]);
             atomicAdd(&g_tc_prof[10], pw[2]);
+            atomicAdd(&g_tc_prof[15], pw[3]);
             atomicAdd(&g_tc_prof[9], (unsigned long long)(t_end - t_loop));
         } else if (warp == 4) {
             atomicAdd(&g_tc_prof[3], pw[0]);
             atomicAdd(&g_tc_prof[4], pw[1]);
+            atomicAdd(&g_tc_prof[13], pw[2]);
+            atomicAdd(&g_tc_prof[14], pw[3]);
         } else if (warp == 8) {
             atomicAdd(&g_tc_prof[5], pw[0]);
             atomicAdd(&g_tc_prof[7], pw[1]);
@@ -723,27 +763,11 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     int tiles = ((g.nx + TC_TW - 1) / TC_TW) * ((g.ny + TC_TH - 1) / TC_TH);
     dim3 grid(tiles, (C + TC_M - 1) / TC_M);
     size_t smem = sizeof(TcSmem);
-    bool dense = p->max_cand > 4096;
-    if (const char* e = getenv("HEGRID_TC_DENSE")) dense = atoi(e) != 0;
-    int promote_every = 16;
-    if (const char* e = getenv("HEGRID_TC_PROMOTE")) promote_every = atoi(e) > 0 ? atoi(e) : 1 << 30;
     int dbg = 0;
     if (const char* e = getenv("HEGRID_TC_DEBUG")) dbg = atoi(e);
-    if (dense) {
-        HG_TRY(cudaFuncSetAttribute(k_accum_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-        k_accum_tc<true><<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched,
-                                                          p->d_tc_tile_off, p->d_tc_wsum, d_v,
-                                                          ldv, C, d_out, d_weight, promote_every,
-                                                          dbg);
-    } else {
-        HG_TRY(cudaFuncSetAttribute(k_accum_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-        k_accum_tc<false><<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched,
-                                                           p->d_tc_tile_off, p->d_tc_wsum, d_v,
-                                                           ldv, C, d_out, d_weight, promote_every,
-                                                           dbg);
-    }
+    HG_TRY(cudaFuncSetAttribute(k_accum_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_accum_tc<<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched, p->d_tc_tile_off,
+                                               p->d_tc_wsum, C, d_out, d_weight, dbg);
     count_launch();
     if (dbg & 32) {
         unsigned long long h[16];
@@ -752,10 +776,11 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
         const double tot = (double)h[0];
         fprintf(stderr, "[tc prof] CTAs %d, cycles/CTA %.0f | issuer: waitA %.2f waitB %.2f issue %.2f | "
                 "A: waitV %.2f waitAempty %.2f | B: waitBempty %.2f waitV %.2f work %.2f | V: waitVempty %.2f | "
-                "epilogue %.2f (fractions of CTA time)\n",
+                "epilogue %.2f | A promote %.2f loadsplit %.2f | issuer wait free %.2f (fractions of CTA time)\n",
                 grid.x * grid.y, tot / (grid.x * grid.y), h[1] / tot, h[2] / tot, h[10] / tot,
-                h[3] / tot, h[4] / tot, h[5] / tot, h[11] / tot, h[7] / tot, h[6] / tot, h[9] / tot);
-        fprintf(stderr, "[tc prof] debug counter: %llu\n", h[12]);
+                h[3] / tot, h[4] / tot, h[5] / tot, h[11] / tot, h[7] / tot, h[6] / tot, h[9] / tot,
+                h[13] / tot, h[14] / tot, h[15] / tot);
+        fprintf(stderr, "[tc prof] max chunks per block %u, segment %d chunks\n", p->tc_max_cpb, SEG);
         unsigned long long z[16] = {0};
         cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
     }

@@ -39,30 +39,24 @@ __device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count));
 }
+// Wait for the phase with the given parity to complete.  try_wait with a suspend-time hint
+// parks the warp in hardware until the phase flips (or the hint expires) instead of
+// spinning on the issue slots the producer warps need.
+#ifndef HG_MBAR_SUSPEND_NS
+#define HG_MBAR_SUSPEND_NS 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t"
         ".reg .pred p;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t"
-        "}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+        "}\n" :: "r"(smem_u32(bar)), "r"(parity), "n"(HG_MBAR_SUSPEND_NS) : "memory");
 }
-
-// Same, with a nanosleep backoff between polls: for roles that usually run ahead and
-// would otherwise spin on the issue slots the SIMT producers need.
+// Kept for the roles that usually run ahead (same wait; the hint already suspends).
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-    uint32_t ok = 0;
-    while (true) {
-        asm volatile(
-            "{\n\t"
-            ".reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t"
-            "}\n" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-        if (ok) break;
-        __nanosleep(64);
-    }
+    mbar_wait(bar, parity);
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
@@ -131,7 +125,7 @@ __device__ __forceinline__ void mma_tf32_ts_warp_acc(uint32_t d_tmem, uint32_t a
 }
 // One run of the 3xTF32 product over a 32-sample chunk: 4 K-steps x (hi*hi, hi*lo, lo*hi),
 // 12 MMAs behind a single elect.  A stage in TMEM: hi at columns a0 + 8 ks, lo at
-// a0 + 32 + 8 ks; B descriptors: hi at b0 + ks * ks_step (16-B units), lo at + lo_off.
+// a0 + 32 + 8 ks; B descriptors: hi at b0 + ks * KS_STEP (16-B units), lo at + LO_OFF.
 // The first MMA accumulates iff acc0 != 0, the other 11 always accumulate.
 template <int KS_STEP, int LO_OFF>
 __device__ __forceinline__ void mma_run_3xtf32(uint32_t d, uint32_t a0, uint64_t b0,
