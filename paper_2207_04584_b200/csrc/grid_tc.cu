@@ -15,7 +15,7 @@
 //   * the per-tile chunk schedule {plan position, n, bin row, mask of reachable blocks}
 //     (Algorithm 1's "determine the region ... of the contribution points",
 //     PAPER.md:209-217, hoisted out of the hot loop);
-//   * W per cell, summed by k_tc_wsum from the very same fp32 weights (patch4x4_weights).
+//   * W per cell, summed by k_tc_wsum from the very same fp32 weights (patch_weights).
 //
 // CTA = 16x16 cells (16 blocks) x 128 channels, 512 threads, warp-specialised:
 //   warp 0 (lane 0) : MMA issuer: per chunk, per run of consecutive in-reach blocks, 4 K-steps
@@ -73,6 +73,7 @@ constexpr int TC_KC = 32;                 // samples per chunk (4 MMA K-steps of
 constexpr int NA = HG_TC_NA;              // A stages (TMEM)
 constexpr int NBS = HG_TC_NBS;            // B stages (SMEM)
 constexpr int NV = HG_TC_NV;              // V staging stages (SMEM)
+static_assert(NA == NBS, "A and B stages are released by one commit");
 constexpr int MAXQ = 8;                   // max blocks (B slots) per chunk entry
 // The tensor core's fp32 accumulation truncates, so its error grows with the number of MMAs
 // accumulated into one D element.  D is therefore double-buffered in TMEM by segments of
@@ -103,7 +104,8 @@ struct TcSmem {
     float4 Gs[NV][TC_KC];                 // the chunk's sample geometry (plan order)
     uint4 Es[NV];                         // the chunk's schedule entry (written by the V loader)
     uint32_t Bmask[NBS];                  // block mask of the chunk in each weight stage
-    uint64_t a_full[NA], a_empty[NA], b_full[NBS], b_empty[NBS], v_full[NV], v_empty[NV];
+    // A stage s and B stage s hold the same chunk (NA == NBS): one commit frees both
+    uint64_t a_full[NA], b_full[NBS], s_empty[NA], v_full[NV], v_empty[NV];
     uint64_t seg_done[2], seg_free[2];    // D buffer d: segment's MMAs complete / promoted
     uint64_t bar_done;
     uint32_t tmem_base;
@@ -192,6 +194,14 @@ __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int ti
             if (n_out) {
 #pragma unroll
                 for (int b = 0; b < TC_NB; ++b) cpb[b] += __popc(__ballot_sync(0xffffffffu, (mk >> b) & 1u));
+                const uint32_t nchunk = __popc(__ballot_sync(0xffffffffu, mk != 0));
+                const uint32_t nblk = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(mk));
+                const uint32_t nsmp = __reduce_add_sync(0xffffffffu, mk ? n : 0u);
+                if (lane == 0) {
+                    atomicAdd(&n_out[tiles + 1], nchunk);
+                    atomicAdd(&n_out[tiles + 2], nblk);
+                    atomicAdd(&n_out[tiles + 3], nsmp);
+                }
             }
             if (mk && sched) {
                 uint32_t pos = base + cnt + incl - ne;
@@ -218,7 +228,7 @@ __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int ti
     }
 }
 
-// W per cell from the tensor-core engine's own weights (patch4x4_weights), two-level sum
+// W per cell from the tensor-core engine's own weights (patch_weights), two-level sum
 // (per bin row, then compensated) in plan order: deterministic.
 __global__ void k_tc_wsum(const __grid_constant__ Geom g, PlanDev pd, float* __restrict__ wsum) {
     const int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -241,7 +251,7 @@ __global__ void k_tc_wsum(const __grid_constant__ Geom g, PlanDev pd, float* __r
                 sv[u] = (uint32_t)u < nv ? pd.geo[s + u] : make_float4(0.0f, kInvalidDy, 0.0f, 0.0f);
             }
             float w[4][4];
-            patch4x4_weights(g, pd, br, j, ci0, cos_c, sv, s, w);
+            patch_weights<4>(g, pd, br, j, ci0, 0, cos_c, sv, s, w);
 #pragma unroll
             for (int u = 0; u < 4; ++u) part += w[u][cc];
         }
@@ -260,14 +270,14 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     const int64_t cells = (int64_t)g.nx * g.ny;
     uint32_t* d_n = nullptr;
     float* d_w = nullptr;
-    HG_TRY(cudaMalloc(&d_n, (tiles + 1) * sizeof(uint32_t)));
+    HG_TRY(cudaMalloc(&d_n, (tiles + 4) * sizeof(uint32_t)));
     cudaError_t e = cudaMalloc(&d_w, cells * sizeof(float));
     if (e != cudaSuccess) {
         cudaFree(d_n);
         return cuda_status(e);
     }
     const int threads = 128, blocks = (tiles * 32 + threads - 1) / threads;
-    e = cudaMemsetAsync(d_n, 0, (tiles + 1) * sizeof(uint32_t), st);
+    e = cudaMemsetAsync(d_n, 0, (tiles + 4) * sizeof(uint32_t), st);
     if (e != cudaSuccess) {
         cudaFree(d_n);
         cudaFree(d_w);
@@ -276,9 +286,9 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     k_tc_schedule<<<blocks, threads, 0, st>>>(g, p->dev(), tiles, d_n, nullptr, nullptr);
     k_tc_wsum<<<(int)((cells + 127) / 128), 128, 0, st>>>(g, p->dev(), d_w);
     count_launch(2);
-    std::vector<uint32_t> h(tiles + 1, 0);
+    std::vector<uint32_t> h(tiles + 4, 0);
     e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d_n, (tiles + 1) * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d_n, (tiles + 4) * 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
         cudaFree(d_n);
@@ -308,6 +318,9 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     p->d_tc_wsum = d_w;
     p->tc_nchunks = total;
     p->tc_max_cpb = h[tiles];
+    p->tc_stats[0] = h[tiles + 1];    // chunks (distinct sample groups)
+    p->tc_stats[1] = h[tiles + 2];    // (chunk, block) pairs
+    p->tc_stats[2] = h[tiles + 3];    // samples over all chunks
     return HEGRID_OK;
 }
 
@@ -342,11 +355,10 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     if (tid == 32) {
         for (int s = 0; s < NA; ++s) {
             tc::mbar_init(&sm.a_full[s], 128);
-            tc::mbar_init(&sm.a_empty[s], 1);
+            tc::mbar_init(&sm.s_empty[s], 1);
         }
         for (int s = 0; s < NBS; ++s) {
             tc::mbar_init(&sm.b_full[s], W_THREADS);
-            tc::mbar_init(&sm.b_empty[s], 1);
         }
         for (int s = 0; s < NV; ++s) {
             tc::mbar_init(&sm.v_full[s], 1);
@@ -449,8 +461,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     q += r;
                 }
             }
-            tc::mma_commit_warp(&sm.a_empty[sa]);
-            tc::mma_commit_warp(&sm.b_empty[sb]);
+            tc::mma_commit_warp(&sm.s_empty[sa]);      // a commit costs ~100 cycles: one per chunk
             if (c % SEG == SEG - 1 || c == nchunks - 1) tc::mma_commit_warp(&sm.seg_done[d]);
             __syncwarp();
             TPROF_END(2);
@@ -508,7 +519,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         // ============================ A producers ============================
         const int q4 = warp & 3;
         const int chl = q4 * 32 + lane;            // channel within the block = TMEM lane
-        const bool ch_ok = cb + chl < C && !(dbg & 4);
+        // channels >= C arrive as zeros (the tensor map's out-of-range fill)
+        const bool ch_ok = !(dbg & 4);
         // Software-pipelined: the values of chunk c+1 are loaded and split while chunk c's
         // tcgen05.st is in flight; chunk c is published (a_full) once its stores completed.
         uint32_t hi[TC_KC], lo[TC_KC];
@@ -523,17 +535,22 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const uint4 ee = sm.Es[sv];
             const uint32_t nk = ee.y & 63;
             if ((c / SEG) & 1) segmask[1] |= ee.z; else segmask[0] |= ee.z;
+            if (nk == TC_KC && ch_ok) {            // full chunk: no masking
 #pragma unroll
-            for (int k = 0; k < TC_KC; ++k) {
-                const float v = ((uint32_t)k < nk && ch_ok) ? vs[k * TC_M] : 0.0f;
-                tc::split_tf32(v, hi[k], lo[k]);
+                for (int k = 0; k < TC_KC; ++k) tc::split_tf32(vs[k * TC_M], hi[k], lo[k]);
+            } else {                                // rows >= nk belong to other chunks
+#pragma unroll
+                for (int k = 0; k < TC_KC; ++k) {
+                    const float v = ((uint32_t)k < nk && ch_ok) ? vs[k * TC_M] : 0.0f;
+                    tc::split_tf32(v, hi[k], lo[k]);
+                }
             }
         };
         auto store = [&](int c) {
             const int sa = c % NA;
             {
                 TPROF_BEGIN;
-                if (c >= NA) tc::mbar_wait(&sm.a_empty[sa], ((c / NA) - 1) & 1);
+                if (c >= NA) tc::mbar_wait(&sm.s_empty[sa], ((c / NA) - 1) & 1);
                 TPROF_END(1);
             }
             tc::fence_after_sync();
@@ -576,8 +593,11 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         }
     } else if (warp >= 8) {
         // ============================ B producers ============================
+        // item = (slot q, cell row rr, column pair ch2, sample quad kq): 4 samples x 2 cells;
+        // a thread keeps (kq, ch2, rr) and takes slots q0 and q0 + 4 (64 items per slot, so
+        // every B warp has work as soon as the chunk reaches 4 blocks)
         const int wt = tid - 8 * 32;                  // 0..255
-        const int kq = wt & 7, rr = (wt >> 3) & 3, q0 = wt >> 5;
+        const int kq = wt & 7, ch2 = (wt >> 3) & 1, rr = (wt >> 4) & 3, q0 = wt >> 6;
         float cosr[TC_BY];                        // cos(lat) of this thread's possible rows
 #pragma unroll
         for (int by = 0; by < TC_BY; ++by) {
@@ -616,14 +636,14 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const int sb = c % NBS;
             {
                 TPROF_BEGIN;
-                if (c >= NBS) tc::mbar_wait(&sm.b_empty[sb], ((c / NBS) - 1) & 1);
+                if (c >= NBS) tc::mbar_wait(&sm.s_empty[sb], ((c / NBS) - 1) & 1);
                 TPROF_END(0);
             }
             TPROF_BEGIN;
             const int nq = (dbg & 1) ? 0 : __popc(mask);
             uint8_t* bst = &sm.B[sb][0];
 #pragma unroll 1
-            for (int q = q0; q < nq; q += 8) {
+            for (int q = q0; q < nq; q += 4) {
                 const int b = (blist >> (4 * q)) & 15;
                 const int by = b / TC_BX;
                 const int cj = j0 + by * 4 + rr;
@@ -633,24 +653,24 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 #pragma unroll
                 for (int k = 1; k < TC_BY; ++k)
                     if (by == k) cos_c = cosr[k];
-                float w[4][4];                 // [sample][cell col]
+                float w[4][2];                 // [sample][cell col]
                 if (dbg & 64) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
 #pragma unroll
-                        for (int cc = 0; cc < 4; ++cc) w[u][cc] = g4[u].x * cos_c + (float)cc;
+                        for (int cc = 0; cc < 2; ++cc) w[u][cc] = g4[u].x * cos_c + (float)cc;
                 } else {
-                    patch4x4_weights(g, pd, row, cj, ci0, cos_c, g4, pstart + 4 * kq, w);
+                    patch_weights<2>(g, pd, row, cj, ci0, 2 * ch2, cos_c, g4, pstart + 4 * kq, w);
                     if (!rok) {
 #pragma unroll
                         for (int u = 0; u < 4; ++u)
 #pragma unroll
-                            for (int cc = 0; cc < 4; ++cc) w[u][cc] = 0.0f;
+                            for (int cc = 0; cc < 2; ++cc) w[u][cc] = 0.0f;
                     }
                 }
 #pragma unroll
-                for (int cc = 0; cc < 4; ++cc) {
-                    const int n = rr * 4 + cc;
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int n = rr * 4 + 2 * ch2 + cc;
                     uint4 h4, l4;
                     tc::split_tf32(w[0][cc], h4.x, l4.x);
                     tc::split_tf32(w[1][cc], h4.y, l4.y);
@@ -780,7 +800,9 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
                 grid.x * grid.y, tot / (grid.x * grid.y), h[1] / tot, h[2] / tot, h[10] / tot,
                 h[3] / tot, h[4] / tot, h[5] / tot, h[11] / tot, h[7] / tot, h[6] / tot, h[9] / tot,
                 h[13] / tot, h[14] / tot, h[15] / tot);
-        fprintf(stderr, "[tc prof] max chunks per block %u, segment %d chunks\n", p->tc_max_cpb, SEG);
+        fprintf(stderr, "[tc prof] max chunks per block %u, segment %d chunks | entries %lld, chunks %u, "
+                "blocks/chunk %.2f, samples/chunk %.1f\n", p->tc_max_cpb, SEG, (long long)p->tc_nchunks,
+                p->tc_stats[0], (double)p->tc_stats[1] / p->tc_stats[0], (double)p->tc_stats[2] / p->tc_stats[0]);
         unsigned long long z[16] = {0};
         cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
     }

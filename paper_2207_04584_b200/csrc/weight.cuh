@@ -88,23 +88,25 @@ __device__ __forceinline__ float pair_weight(const Geom& g, const PlanDev& pd, i
     return in ? ex2_approx(d2 * g.neg_k2) : 0.0f;
 }
 
-// Weights of a 4x4 (sample x cell) patch: samples s[0..3] (plan positions p0..p0+3)
-// against 4 consecutive cells ci0 .. ci0+3 of cell row cj, sharing the per-sample terms
-// (sin^2(dlat/2), cos products, lon offset) between the 4 cells.  Same predicate as
+// Weights of a 4 x NCOL (sample x cell) patch: samples s[0..3] (plan positions p0..p0+3)
+// against the NCOL consecutive cells ci0 + c0 .. ci0 + c0 + NCOL - 1 of cell row cj (ci0 =
+// the 4-aligned first column of the cell block, c0 + NCOL <= 4), sharing the per-sample
+// terms (sin^2(dlat/2), cos products, lon offset) between the cells.  Same predicate as
 // pair_weight (fp32 outside the guard band, fp64 haversine inside; the rare recheck sits
 // behind one branch per patch).  Invalid samples must arrive as {0, 1e18, 0, 0} (their d^2
 // is clamped to a 1-radian offset, far outside any support: weight 0); cells >= nx get
-// weight 0.  ci0 is the 4-aligned column of the
-// cell block.  Used by the tensor-core engine's B producers and by the plan's W kernel,
-// so both see bit-identical weights.  w[u][cc].
+// weight 0.  Every weight is computed by the same expression whatever NCOL and c0, so the
+// tensor-core engine's B producers (4 x 2 patches) and the plan's W kernel (4 x 4) see
+// bit-identical weights.  w[u][j] is the weight of sample u and cell column c0 + j.
 constexpr float kInvalidDy = 1e18f;
-__device__ __forceinline__ void patch4x4_weights(const Geom& g, const PlanDev& pd, int br, int cj,
-                                                 int ci0, float cos_c, const float4 (&s)[4],
-                                                 uint32_t p0, float (&w)[4][4]) {
+template <int NCOL>
+__device__ __forceinline__ void patch_weights(const Geom& g, const PlanDev& pd, int br, int cj,
+                                              int ci0, int c0, float cos_c, const float4 (&s)[4],
+                                              uint32_t p0, float (&w)[4][NCOL]) {
     const float hlon = 0.5f * g.dlon_rad, hlat = 0.5f * g.dlat_rad;
     const float fy = (float)(br - g.mlat - cj);
     const int ix = -g.mlon - ci0;
-    uint32_t band = 0;      // bit 4u + cc: pair inside the guard band
+    uint32_t band = 0;      // bit NCOL u + j: pair inside the guard band
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const float a = fminf(fabsf((fy + s[u].y) * hlat), 1.0f);
@@ -113,41 +115,38 @@ __device__ __forceinline__ void patch4x4_weights(const Geom& g, const PlanDev& p
         const float ccs = cos_c * s[u].z;
         const float b0 = ((float)(__float_as_int(s[u].w) + ix) + s[u].x) * hlon;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-            const float bb = b0 - (float)cc * hlon;
+        for (int j = 0; j < NCOL; ++j) {
+            const float bb = b0 - (float)(c0 + j) * hlon;
             const float b2 = bb * bb;
             const float sbv = fmaf(b2 * (-1.0f / 3.0f), b2, b2);
             const float h = fmaf(ccs, sbv, sa);
             // 4 asin^2(sqrt h) = h (4 + 4h/3 + 32h^2/45 + ...)
             const float d2 = h * fmaf(h, fmaf(h, 32.0f / 45.0f, 4.0f / 3.0f), 4.0f);
-            band |= (uint32_t)((d2 > g.R2_lo) & (d2 <= g.R2_hi)) << (4 * u + cc);
+            band |= (uint32_t)((d2 > g.R2_lo) & (d2 <= g.R2_hi)) << (NCOL * u + j);
             const float e = ex2_approx(d2 * g.neg_k2);
-            w[u][cc] = d2 <= g.R2_hi ? e : 0.0f;     // band pairs provisionally in
+            w[u][j] = d2 <= g.R2_hi ? e : 0.0f;     // band pairs provisionally in
         }
     }
-#ifdef HG_W_NORECHECK
-    band = 0;
-#endif
     if (band) {   // rare: decide the guard-band pairs in fp64 (one call site, no array indexing)
         uint32_t kill = 0;
 #pragma unroll 1
         for (uint32_t m = band; m; m &= m - 1) {
-            const int k = __ffs(m) - 1, u = k >> 2, cc = k & 3;
+            const int k = __ffs(m) - 1, u = k / NCOL, cc = c0 + k % NCOL;
             if (ci0 + cc < g.nx) {
                 const double2 ll = pd.ll[p0 + u];
                 if (!support_fp64(g, ci0 + cc, cj, ll.x, ll.y)) kill |= 1u << k;
             }
         }
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if ((kill >> k) & 1u) w[k >> 2][k & 3] = 0.0f;
+        for (int k = 0; k < 4 * NCOL; ++k)
+            if ((kill >> k) & 1u) w[k / NCOL][k % NCOL] = 0.0f;
     }
-    if (ci0 + 4 > g.nx) {
+    if (ci0 + c0 + NCOL > g.nx) {
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-            if (ci0 + cc >= g.nx)
+        for (int j = 0; j < NCOL; ++j)
+            if (ci0 + c0 + j >= g.nx)
 #pragma unroll
-                for (int u = 0; u < 4; ++u) w[u][cc] = 0.0f;
+                for (int u = 0; u < 4; ++u) w[u][j] = 0.0f;
     }
 }
 

@@ -8,13 +8,13 @@
 
 using namespace hg;
 
-__global__ void k_bench(int r, int runs_per_chunk, int chunks, int st_interfere, unsigned long long* out) {
+__global__ void k_bench(int r, int runs_per_chunk, int chunks, int st_interfere, int commits, unsigned long long* out) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t tbase;
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, cb[4];
     const int warp = threadIdx.x >> 5;
     if (warp == 0) tc::tmem_alloc(&tbase, 512);
-    if (threadIdx.x == 32) { tc::mbar_init(&bar, 1); asm volatile("fence.mbarrier_init.release.cluster;"); }
+    if (threadIdx.x == 32) { tc::mbar_init(&bar, 1); for (int i = 0; i < 4; ++i) tc::mbar_init(&cb[i], 1); asm volatile("fence.mbarrier_init.release.cluster;"); }
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
@@ -27,6 +27,7 @@ __global__ void k_bench(int r, int runs_per_chunk, int chunks, int st_interfere,
             const uint32_t a0 = t + 256 + (c & 3) * 64;
             for (int k = 0; k < runs_per_chunk; ++k)
                 tc::mma_run_3xtf32<2, 1024>(t + (uint32_t)(k * 16 * r) % 256u, a0, d0 + (uint64_t)(k * r * 128), idesc, 1);
+            for (int k = 0; k < commits; ++k) tc::mma_commit_warp(&cb[k]);
         }
         long long t1 = clock64();
         tc::mma_commit_warp(&bar);
@@ -50,15 +51,15 @@ int main() {
     unsigned long long* d;
     cudaMalloc(&d, 16);
     cudaFuncSetAttribute(k_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    for (int st : {0, 1}) {
-        for (int r : {1, 2, 3, 4, 6, 8}) {
-            int chunks = 256, rpc = 2;
-            k_bench<<<148, 256, 64 * 1024>>>(r, rpc, chunks, st, d);
+    for (int cm : {0, 2, 3}) {
+        for (int r : {1, 2, 3, 4}) {
+            int chunks = 256, rpc = 2, st = 1;
+            k_bench<<<148, 256, 64 * 1024>>>(r, rpc, chunks, st, cm, d);
             cudaError_t e = cudaDeviceSynchronize();
             unsigned long long h[2];
             cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
             double n = (double)chunks * rpc * 12;
-            printf("st=%d r=%d N=%3d: issue %.1f cyc/mma, complete %.1f cyc/mma, %.0f MAC/cyc %s\n", st, r, 16 * r,
+            printf("commits=%d r=%d N=%3d: issue %.1f cyc/mma, complete %.1f cyc/mma, %.0f MAC/cyc %s\n", cm, r, 16 * r,
                    h[0] / n, h[1] / n, 128.0 * 16 * r * 8 / (h[1] / n), e == cudaSuccess ? "" : cudaGetErrorString(e));
         }
     }
