@@ -76,7 +76,7 @@ struct hegrid_plan_s {
     mutable uint32_t* d_tc_tile_off = nullptr; // [tiles + 1]
     mutable int64_t tc_nchunks = -1;
     mutable uint32_t tc_max_cpb = 0;           // max schedule entries touching one block
-    mutable uint32_t tc_stats[3] = {0, 0, 0};  // chunks, (chunk, block) pairs, samples
+    mutable uint32_t tc_stats[5] = {0, 0, 0, 0, 0};  // chunks, (chunk, block) pairs, samples, runs, spans
     mutable float* d_tc_wsum = nullptr;        // [cells] W with the TC engine's weights
     // scratch for USER_CN device grids
     float* d_scratch = nullptr;

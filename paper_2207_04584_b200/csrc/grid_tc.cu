@@ -197,10 +197,14 @@ __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int ti
                 const uint32_t nchunk = __popc(__ballot_sync(0xffffffffu, mk != 0));
                 const uint32_t nblk = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(mk));
                 const uint32_t nsmp = __reduce_add_sync(0xffffffffu, mk ? n : 0u);
+                const uint32_t nrun = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(mk & ~(mk << 1)));
+                const uint32_t nspan = __reduce_add_sync(0xffffffffu, mk ? (uint32_t)(32 - __clz(mk) - __ffs(mk) + 1) : 0u);
                 if (lane == 0) {
                     atomicAdd(&n_out[tiles + 1], nchunk);
                     atomicAdd(&n_out[tiles + 2], nblk);
                     atomicAdd(&n_out[tiles + 3], nsmp);
+                    atomicAdd(&n_out[tiles + 4], nrun);
+                    atomicAdd(&n_out[tiles + 5], nspan);
                 }
             }
             if (mk && sched) {
@@ -270,14 +274,14 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     const int64_t cells = (int64_t)g.nx * g.ny;
     uint32_t* d_n = nullptr;
     float* d_w = nullptr;
-    HG_TRY(cudaMalloc(&d_n, (tiles + 4) * sizeof(uint32_t)));
+    HG_TRY(cudaMalloc(&d_n, (tiles + 6) * sizeof(uint32_t)));
     cudaError_t e = cudaMalloc(&d_w, cells * sizeof(float));
     if (e != cudaSuccess) {
         cudaFree(d_n);
         return cuda_status(e);
     }
     const int threads = 128, blocks = (tiles * 32 + threads - 1) / threads;
-    e = cudaMemsetAsync(d_n, 0, (tiles + 4) * sizeof(uint32_t), st);
+    e = cudaMemsetAsync(d_n, 0, (tiles + 6) * sizeof(uint32_t), st);
     if (e != cudaSuccess) {
         cudaFree(d_n);
         cudaFree(d_w);
@@ -286,9 +290,9 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     k_tc_schedule<<<blocks, threads, 0, st>>>(g, p->dev(), tiles, d_n, nullptr, nullptr);
     k_tc_wsum<<<(int)((cells + 127) / 128), 128, 0, st>>>(g, p->dev(), d_w);
     count_launch(2);
-    std::vector<uint32_t> h(tiles + 4, 0);
+    std::vector<uint32_t> h(tiles + 6, 0);
     e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d_n, (tiles + 4) * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d_n, (tiles + 6) * 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
         cudaFree(d_n);
@@ -321,6 +325,8 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     p->tc_stats[0] = h[tiles + 1];    // chunks (distinct sample groups)
     p->tc_stats[1] = h[tiles + 2];    // (chunk, block) pairs
     p->tc_stats[2] = h[tiles + 3];    // samples over all chunks
+    p->tc_stats[3] = h[tiles + 4];    // runs of consecutive blocks
+    p->tc_stats[4] = h[tiles + 5];    // block spans
     return HEGRID_OK;
 }
 
@@ -379,17 +385,37 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = sm.tmem_base;
+    if (warp >= 4 && warp < 8) {      // both D buffers start at 0 (every MMA accumulates)
+        uint32_t z[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) z[k] = 0u;
+#pragma unroll
+        for (int c0 = 0; c0 < (int)A_COL0; c0 += 32)
+            tc::tmem_st32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, z);
+        tc::wait_st();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
 
-    // D buffer d -> master: this warp's lane quarter (channels), blocks in `mask`
-    auto promote_buffer = [&](int d, uint32_t mask) {
+    // D buffer d -> master: this warp's lane quarter (channels), blocks in `mask`; with
+    // rezero, the blocks are cleared for the buffer's next segment
+    auto promote_buffer = [&](int d, uint32_t mask, bool rezero) {
         const int q4 = warp & 3, row = q4 * 32 + lane;
         float* mrow = &sm.M[row][0];
         while (mask) {
             const int b = __ffs(mask) - 1;
             mask &= mask - 1;
             uint32_t r[16];
-            tc::tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)d * D_COLS + (uint32_t)(b * TC_N), r);
+            const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)d * D_COLS + (uint32_t)(b * TC_N);
+            tc::tmem_ld16(ta, r);
             tc::wait_ld();
+            if (rezero) {
+                uint32_t z16[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) z16[k] = 0u;
+                tc::tmem_st16(ta, z16);
+            }
             const int x0 = (b % TC_BX) * 4, y0 = (b / TC_BX) * 4;
 #pragma unroll
             for (int cy = 0; cy < 4; ++cy) {
@@ -411,19 +437,17 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 
     if (warp == 0) {
         // ============================ MMA issuer =============================
-        uint32_t touched = 0;
         for (int c = 0; c < nchunks; ++c) {
             const int seg = c / SEG, d = seg & 1;
             if (c % SEG == 0) {
-                // a new segment restarts D buffer d (accumulate = 0 on each block's first
-                // MMA); its previous contents (segment seg - 2) must have been promoted
+                // a new segment accumulates into D buffer d, which the A warps have promoted
+                // (segment seg - 2) and zeroed
                 if (seg >= 2) {
                     TPROF_BEGIN;
                     tc::mbar_wait(&sm.seg_free[d], ((seg >> 1) - 1) & 1);
                     TPROF_END(3);
                     tc::fence_after_sync();
                 }
-                touched = 0;
             }
             const int sa = c % NA, sb = c % NBS;
             {
@@ -440,24 +464,21 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const uint32_t mask = sm.Bmask[sb];
             TPROF_BEGIN;
             if (!(dbg & 2)) {
-                // whole warp walks the runs (uniform values); each run is one 12-MMA block
-                // behind a single elect; descriptors advance by (byte offset >> 4)
+                // runs of consecutive in-reach blocks = consecutive B slots (slots follow the
+                // mask order); D buffers are zeroed before each segment, so every MMA
+                // accumulates.  Each run is 12 MMAs behind one elect.
                 const uint64_t dh0 = tc::sdesc_sw128(tc::smem_u32(&sm.B[sb][0]));
                 const uint32_t a0 = tmem + A_COL0 + sa * 64;
                 const uint32_t dbase = tmem + (uint32_t)d * D_COLS;
                 uint32_t mm = mask;
                 int q = 0;
                 while (mm) {
-                    // run of consecutive in-reach blocks [b, b + r) with the same D state
                     const int b = __ffs(mm) - 1;
-                    const uint32_t tb = (touched >> b) & 1u;
-                    const uint32_t same = mm & (tb ? touched : ~touched);
-                    const int r = __ffs(~(same >> b)) - 1;
+                    const int r = __ffs(~(mm >> b)) - 1;
                     mm &= ~(((1u << r) - 1u) << b);
                     tc::mma_run_3xtf32<(32 >> 4), (B_HALF >> 4)>(
                         dbase + (uint32_t)(b * TC_N), a0, dh0 + (uint64_t)((q * TC_N * B_ROW) >> 4),
-                        tc::idesc_tf32(TC_M, TC_N * r), tb);
-                    touched |= ((1u << r) - 1u) << b;
+                        tc::idesc_tf32(TC_M, TC_N * r), 1u);
                     q += r;
                 }
             }
@@ -582,8 +603,9 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     TPROF_BEGIN;
                     tc::mbar_wait(&sm.seg_done[d], (s >> 1) & 1);
                     tc::fence_after_sync();
-                    promote_buffer(d, segmask[d]);
+                    promote_buffer(d, segmask[d], true);
                     segmask[d] = 0;
+                    tc::wait_st();
                     tc::fence_before_sync();
                     tc::mbar_arrive(&sm.seg_free[d]);
                     TPROF_END(2);
@@ -640,6 +662,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 TPROF_END(0);
             }
             TPROF_BEGIN;
+            // slot q holds the q-th in-reach block of the entry (mask order, blist)
             const int nq = (dbg & 1) ? 0 : __popc(mask);
             uint8_t* bst = &sm.B[sb][0];
 #pragma unroll 1
@@ -696,7 +719,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     tc::fence_after_sync();
     if (warp >= 4 && warp < 8) {
         for (int s = (nseg >= 2 ? nseg - 2 : 0); s < nseg; ++s)
-            if (!promoted_in_loop(s)) promote_buffer(s & 1, segmask[s & 1]);
+            if (!promoted_in_loop(s)) promote_buffer(s & 1, segmask[s & 1], false);
     }
     __syncthreads();
     {
@@ -801,8 +824,10 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
                 h[3] / tot, h[4] / tot, h[5] / tot, h[11] / tot, h[7] / tot, h[6] / tot, h[9] / tot,
                 h[13] / tot, h[14] / tot, h[15] / tot);
         fprintf(stderr, "[tc prof] max chunks per block %u, segment %d chunks | entries %lld, chunks %u, "
-                "blocks/chunk %.2f, samples/chunk %.1f\n", p->tc_max_cpb, SEG, (long long)p->tc_nchunks,
-                p->tc_stats[0], (double)p->tc_stats[1] / p->tc_stats[0], (double)p->tc_stats[2] / p->tc_stats[0]);
+                "blocks/chunk %.2f, samples/chunk %.1f, runs/chunk %.2f, span/chunk %.2f\n", p->tc_max_cpb, SEG,
+                (long long)p->tc_nchunks, p->tc_stats[0], (double)p->tc_stats[1] / p->tc_stats[0],
+                (double)p->tc_stats[2] / p->tc_stats[0], (double)p->tc_stats[3] / p->tc_stats[0],
+                (double)p->tc_stats[4] / p->tc_stats[0]);
         unsigned long long z[16] = {0};
         cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
     }
