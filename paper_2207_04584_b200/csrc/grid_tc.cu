@@ -535,7 +535,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         }
     }
     // A producers keep the block masks of the (at most two) segments not yet promoted
-    uint32_t segmask[2] = {0u, 0u};
+    uint32_t segmask0 = 0u, segmask1 = 0u;   // (scalars: no local-memory array)
     if (warp >= 4 && warp < 8) {
         // ============================ A producers ============================
         const int q4 = warp & 3;
@@ -555,7 +555,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const float* vs = reinterpret_cast<const float*>(&sm.Vs[sv][0]) + chl;
             const uint4 ee = sm.Es[sv];
             const uint32_t nk = ee.y & 63;
-            if ((c / SEG) & 1) segmask[1] |= ee.z; else segmask[0] |= ee.z;
+            if ((c / SEG) & 1) segmask1 |= ee.z; else segmask0 |= ee.z;
             if (nk == TC_KC && ch_ok) {            // full chunk: no masking
 #pragma unroll
                 for (int k = 0; k < TC_KC; ++k) tc::split_tf32(vs[k * TC_M], hi[k], lo[k]);
@@ -603,8 +603,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     TPROF_BEGIN;
                     tc::mbar_wait(&sm.seg_done[d], (s >> 1) & 1);
                     tc::fence_after_sync();
-                    promote_buffer(d, segmask[d], true);
-                    segmask[d] = 0;
+                    promote_buffer(d, d ? segmask1 : segmask0, true);
+                    if (d) segmask1 = 0; else segmask0 = 0;
                     tc::wait_st();
                     tc::fence_before_sync();
                     tc::mbar_arrive(&sm.seg_free[d]);
@@ -719,7 +719,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     tc::fence_after_sync();
     if (warp >= 4 && warp < 8) {
         for (int s = (nseg >= 2 ? nseg - 2 : 0); s < nseg; ++s)
-            if (!promoted_in_loop(s)) promote_buffer(s & 1, segmask[s & 1], false);
+            if (!promoted_in_loop(s)) promote_buffer(s & 1, (s & 1) ? segmask1 : segmask0, false);
     }
     __syncthreads();
     {

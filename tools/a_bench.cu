@@ -24,13 +24,18 @@ __global__ void k(int mode, int iters, unsigned long long* out) {
     for (int c = 0; c < iters; ++c) {
         uint32_t hi[32], lo[32];
         const float* vs = V + (c % 5) * 4096 + chl;
+        if (mode >= 3) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) { hi[k] = c + k; lo[k] = c - k; }
+        } else {
 #pragma unroll
         for (int k = 0; k < 32; ++k) tc::split_tf32(vs[k * 128], hi[k], lo[k]);
+        }
         if (mode >= 1) {
             const uint32_t ta = t + ((uint32_t)((warp & 3) * 32) << 16) + 256 + (c & 3) * 64;
             tc::tmem_st32(ta, hi);
             tc::tmem_st32(ta + 32, lo);
-            if (mode >= 2) tc::wait_st();
+            if (mode == 2 || mode == 4) tc::wait_st();
         } else {
 #pragma unroll
             for (int k = 0; k < 32; ++k) acc += hi[k] ^ lo[k];
@@ -47,11 +52,11 @@ __global__ void k(int mode, int iters, unsigned long long* out) {
 int main() {
     unsigned long long* d; cudaMalloc(&d, 128);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    for (int mode : {0, 1, 2}) {
+    for (int mode : {0, 1, 2, 3, 4}) {
         int iters = 2000;
         k<<<148, 128, 90 * 1024>>>(mode, iters, d);
         cudaError_t e = cudaDeviceSynchronize();
         unsigned long long h[4]; cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
-        printf("mode %d (0 split only, 1 +st, 2 +wait::st): %.1f cycles/chunk %s\n", mode, (double)h[0] / iters, e ? cudaGetErrorString(e) : "");
+        printf("mode %d (0 split, 1 +st, 2 +wait::st, 3 st only, 4 st+wait): %.1f cycles/chunk %s\n", mode, (double)h[0] / iters, e ? cudaGetErrorString(e) : "");
     }
 }

@@ -1,6 +1,6 @@
 timeout 300 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -1
-for m in "0 16" "1 8"; do set -- $m; HEGRID_TC_DENSE=$1 HEGRID_TC_PROMOTE=$2 timeout 120 python tools/det_small.py sparse 2>&1 | tail -1; done
-timeout 120 python tools/det_small.py dense 2>&1 | tail -1
-timeout 300 python tools/diag_tc_dense.py 2>&1 | grep -E "^tc|^simt"
-timeout 800 python tools/err_report.py cfg2 cfg4
-bash tools/tc_ablate.sh 2>&1 | grep dbg | head -2
+for d in 0 3; do
+  t=$(HEGRID_TC_DEBUG=$d python bench.py --steps 3 --warmup 2 --no-cpu --no-e2e --engine tc 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(round(d["ms_per_step"],2))')
+  p=$(HEGRID_TC_DEBUG=$((d+32)) timeout 120 python tools/profile_run.py --workload cfg4 --channels 1024 --engine tc --launches 1 2>&1 | grep "tc prof" | head -1| cut -c1-400)
+  echo "dbg=$d $t ms | $p"
+done
