@@ -340,12 +340,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap tmap_v,
            PlanDev pd, const uint4* __restrict__ sched,
            const uint32_t* __restrict__ tile_off, const float* __restrict__ wsum,
-           int C, float* __restrict__ out, float* __restrict__ wout, int dbg) {
+           int C, float* __restrict__ out, float* __restrict__ wout, int dbg_in) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_raw);
     if (tc::smem_u32(smem_raw) & 1023u) __trap();   // swizzle atoms need 1024-B alignment
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef HG_TC_PROF
+    // debug switches (HEGRID_TC_DEBUG) and cycle counters: only in profiling builds
+    const int dbg = dbg_in;
     const bool prof = (dbg & 32) != 0;
+#else
+    constexpr int dbg = 0;
+    constexpr bool prof = false;
+    (void)dbg_in;
+#endif
     const long long t_start = clock64();
     unsigned long long pw[4] = {0, 0, 0, 0};
 #define TPROF_BEGIN long long _t0 = prof ? clock64() : 0

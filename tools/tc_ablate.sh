@@ -1,4 +1,6 @@
 #!/bin/bash
+# needs the profiling build: tools/build_variant.sh prof -DHG_TC_PROF
+export HEGRID_LIB=${HEGRID_LIB:-tmp_libs/lib_prof.so}
 # time the TC kernel with parts disabled (HEGRID_TC_DEBUG bits: 1 = no B work, 2 = no MMAs,
 # 4 = no A values, 8 = no V copies, 64 = trivial weights) and print the profile split
 for d in 0 1 2 64 3 9; do
