@@ -68,7 +68,10 @@ constexpr int TC_KC = 32;                 // samples per chunk (4 MMA K-steps of
 #define HG_TC_NV 3
 #endif
 #ifndef HG_TC_SEG
-#define HG_TC_SEG 8
+#define HG_TC_SEG 8         // segment length for dense plans
+#endif
+#ifndef HG_TC_SEG_SPARSE
+#define HG_TC_SEG_SPARSE 16 // segment length when no block gets more than TC_CPB_SPARSE chunks
 #endif
 constexpr int NA = HG_TC_NA;              // A stages (TMEM)
 constexpr int NBS = HG_TC_NBS;            // B stages (SMEM)
@@ -79,12 +82,15 @@ constexpr int MAXQ = 8;                   // max blocks (B slots) per chunk entr
 // accumulated into one D element.  D is therefore double-buffered in TMEM by segments of
 // SEG chunks: while the tensor core accumulates segment s+1 into one buffer, the A warps add
 // segment s's buffer into an fp32 master tile in shared memory (round-to-nearest).
-constexpr int SEG = HG_TC_SEG;
+constexpr int SEG_DENSE = HG_TC_SEG, SEG_SPARSE = HG_TC_SEG_SPARSE;
+// A block touched by at most this many chunks in the whole tile accumulates few enough MMAs
+// per segment at SEG_SPARSE (measured: max rel err 4e-6 at cfg4, where the max is 70)
+constexpr uint32_t TC_CPB_SPARSE = 80;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t D_COLS = TC_NB * TC_N;      // one accumulator buffer: 12 blocks x 16 columns
 constexpr uint32_t A_COL0 = 2 * D_COLS;        // 384: A stages after the two D buffers
 static_assert(A_COL0 + NA * 64 <= TMEM_COLS, "TMEM budget");
-static_assert(SEG > NA, "a segment is promoted NA chunks into the next one");
+static_assert(SEG_DENSE > NA && SEG_SPARSE > NA, "a segment is promoted NA chunks into the next one");
 // B stage layout (per hi / lo half): K-major, 128-byte swizzle.  Row R = 16 q + n (slot q,
 // cell n) holds the chunk's 32 tf32 weights (128 B); 8-row groups are 1024-B swizzle atoms
 // (SBO = 1024); the 16-B k-quad j of row R sits at chunk position j ^ (R & 7), so the 32
@@ -336,6 +342,7 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
 __device__ unsigned long long g_tc_prof[16];
 
 // ------------------------------------------------------------------ the kernel
+template <int SEG>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap tmap_v,
            PlanDev pd, const uint4* __restrict__ sched,
@@ -816,9 +823,12 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     size_t smem = sizeof(TcSmem);
     int dbg = 0;
     if (const char* e = getenv("HEGRID_TC_DEBUG")) dbg = atoi(e);
-    HG_TRY(cudaFuncSetAttribute(k_accum_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_accum_tc<<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched, p->d_tc_tile_off,
-                                               p->d_tc_wsum, C, d_out, d_weight, dbg);
+    const bool sparse = p->tc_max_cpb <= TC_CPB_SPARSE;
+    const int SEG = sparse ? SEG_SPARSE : SEG_DENSE;
+    auto kern = sparse ? k_accum_tc<SEG_SPARSE> : k_accum_tc<SEG_DENSE>;
+    HG_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched, p->d_tc_tile_off,
+                                         p->d_tc_wsum, C, d_out, d_weight, dbg);
     count_launch();
     if (dbg & 32) {
         unsigned long long h[16];
