@@ -34,6 +34,10 @@ struct Geom {
     float dlon_rad, dlat_rad;   // cdelt in radians (signed)
     float R2_lo, R2_hi;         // guard band around R^2 (rad^2): below -> in, above -> out
     float neg_k2;               // -log2(e) / (2 sigma^2)  (w = 2^(d^2 * neg_k2))
+    // the same, folded into the exponent t = neg_k2 d^2 = h (K0 + h (K1 + h K2)) of the
+    // tensor-core engine's weight patches; t >= t_in: inside, t < t_out: outside, else the
+    // guard band (t_in = neg_k2 R2_lo, t_out = neg_k2 R2_hi; neg_k2 < 0 flips the order)
+    float tK0, tK1, tK2, t_in, t_out;
 };
 
 // Per-sample plan data in plan order.

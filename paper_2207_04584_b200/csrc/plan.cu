@@ -289,7 +289,13 @@ static hegrid_status make_geom(hegrid_plan_s* p, std::vector<int>& mrow,
     double R2 = g.R_rad * g.R_rad;
     g.R2_lo = (float)(R2 * (1.0 - 1e-5));
     g.R2_hi = (float)(R2 * (1.0 + 1e-5));
-    g.neg_k2 = (float)(-1.0 / (2.0 * g.sigma_rad * g.sigma_rad) / log(2.0));
+    const double nk2 = -1.0 / (2.0 * g.sigma_rad * g.sigma_rad) / log(2.0);
+    g.neg_k2 = (float)nk2;
+    g.tK0 = (float)(4.0 * nk2);
+    g.tK1 = (float)(4.0 / 3.0 * nk2);
+    g.tK2 = (float)(32.0 / 45.0 * nk2);
+    g.t_in = (float)(nk2 * R2 * (1.0 - 1e-5));
+    g.t_out = (float)(nk2 * R2 * (1.0 + 1e-5));
     return HEGRID_OK;
 }
 

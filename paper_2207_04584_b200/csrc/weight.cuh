@@ -106,7 +106,9 @@ __device__ __forceinline__ void patch_weights(const Geom& g, const PlanDev& pd, 
     const float hlon = 0.5f * g.dlon_rad, hlat = 0.5f * g.dlat_rad;
     const float fy = (float)(br - g.mlat - cj);
     const int ix = -g.mlon - ci0;
-    uint32_t band = 0;      // bit NCOL u + j: pair inside the guard band
+    uint32_t kill = 0;      // bit NCOL u + j: band pair outside the fp64 support
+    // exponent t = neg_k2 * d^2 with d^2 = 4 asin^2(sqrt h) = h (4 + 4h/3 + 32h^2/45 + ...)
+    bool band = false;      // some pair inside the guard band
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const float a = fminf(fabsf((fy + s[u].y) * hlat), 1.0f);
@@ -120,19 +122,28 @@ __device__ __forceinline__ void patch_weights(const Geom& g, const PlanDev& pd, 
             const float b2 = bb * bb;
             const float sbv = fmaf(b2 * (-1.0f / 3.0f), b2, b2);
             const float h = fmaf(ccs, sbv, sa);
-            // 4 asin^2(sqrt h) = h (4 + 4h/3 + 32h^2/45 + ...)
-            const float d2 = h * fmaf(h, fmaf(h, 32.0f / 45.0f, 4.0f / 3.0f), 4.0f);
-            band |= (uint32_t)((d2 > g.R2_lo) & (d2 <= g.R2_hi)) << (NCOL * u + j);
-            const float e = ex2_approx(d2 * g.neg_k2);
-            w[u][j] = d2 <= g.R2_hi ? e : 0.0f;     // band pairs provisionally in
+            const float t = h * fmaf(h, fmaf(h, g.tK2, g.tK1), g.tK0);
+            band |= (t < g.t_in) & (t >= g.t_out);
+            w[u][j] = t >= g.t_out ? ex2_approx(t) : 0.0f;     // band pairs provisionally in
         }
     }
-    if (band) {   // rare: decide the guard-band pairs in fp64 (one call site, no array indexing)
-        uint32_t kill = 0;
+    if (band) {   // rare: find the guard-band pairs again and decide them in fp64
 #pragma unroll 1
-        for (uint32_t m = band; m; m &= m - 1) {
-            const int k = __ffs(m) - 1, u = k / NCOL, cc = c0 + k % NCOL;
-            if (ci0 + cc < g.nx) {
+        for (int k = 0; k < 4 * NCOL; ++k) {
+            const int u = k / NCOL, cc = c0 + k % NCOL;
+            // (selects, not s[u]: a dynamic index would put s in local memory)
+            const float4 su = u == 0 ? s[0] : (u == 1 ? s[1] : (u == 2 ? s[2] : s[3]));
+            const float a = fminf(fabsf((fy + su.y) * hlat), 1.0f);
+            const float a2 = a * a;
+            const float sa = fmaf(a2 * (-1.0f / 3.0f), a2, a2);
+            const float ccs = cos_c * su.z;
+            const float b0 = ((float)(__float_as_int(su.w) + ix) + su.x) * hlon;
+            const float bb = b0 - (float)cc * hlon;
+            const float b2 = bb * bb;
+            const float sbv = fmaf(b2 * (-1.0f / 3.0f), b2, b2);
+            const float h = fmaf(ccs, sbv, sa);
+            const float t = h * fmaf(h, fmaf(h, g.tK2, g.tK1), g.tK0);
+            if (t < g.t_in && t >= g.t_out && ci0 + cc < g.nx) {
                 const double2 ll = pd.ll[p0 + u];
                 if (!support_fp64(g, ci0 + cc, cj, ll.x, ll.y)) kill |= 1u << k;
             }
