@@ -175,6 +175,8 @@ void hegrid_plan_destroy(hegrid_plan_t p) {
     cudaFree(p->d_tc_sched);
     cudaFree(p->d_tc_tile_off);
     cudaFree(p->d_tc_wsum);
+    cudaFree(p->d_tc_wimg);
+    cudaFree(p->d_tc_wslot);
     for (auto e : p->prof_events) cudaEventDestroy(e);
     delete p;
 }

@@ -82,6 +82,12 @@ struct hegrid_plan_s {
     mutable uint32_t tc_max_cpb = 0;           // max schedule entries touching one block
     mutable uint32_t tc_stats[5] = {0, 0, 0, 0, 0};  // chunks, (chunk, block) pairs, samples, runs, spans
     mutable float* d_tc_wsum = nullptr;        // [cells] W with the TC engine's weights
+    // precomputed weight image (grid_tc.cu, "PW" mode): per schedule entry, its in-reach
+    // blocks' tf32 hi then lo weights in the shared-memory operand layout (4 KB per block)
+    mutable uint8_t* d_tc_wimg = nullptr;
+    mutable uint32_t* d_tc_wslot = nullptr;    // [entries] first 4-KB slot of each entry
+    mutable int tc_pw = -1;                    // -1 not built, 0 unavailable, 1 built
+    mutable int64_t tc_wimg_bytes = 0;
     // scratch for USER_CN device grids
     float* d_scratch = nullptr;
     size_t scratch_bytes = 0;

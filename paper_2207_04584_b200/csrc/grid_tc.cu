@@ -86,6 +86,8 @@ constexpr int SEG_DENSE = HG_TC_SEG, SEG_SPARSE = HG_TC_SEG_SPARSE;
 // A block touched by at most this many chunks in the whole tile accumulates few enough MMAs
 // per segment at SEG_SPARSE (measured: max rel err 4e-6 at cfg4, where the max is 70)
 constexpr uint32_t TC_CPB_SPARSE = 80;
+// PW mode (precomputed weight image) from this many 128-channel blocks per launch
+constexpr unsigned TC_PW_MIN_CBLOCKS = 4;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t D_COLS = TC_NB * TC_N;      // one accumulator buffer: 12 blocks x 16 columns
 constexpr uint32_t A_COL0 = 2 * D_COLS;        // 384: A stages after the two D buffers
@@ -103,15 +105,25 @@ constexpr int V_ROW = TC_M * 4;                      // 512 B
 constexpr int V_STAGE = TC_KC * V_ROW;               // 16 KB
 constexpr int W_THREADS = 256;            // B producers (warps 8-15)
 constexpr int T_LD = TC_TW * TC_TH + 4;   // epilogue tile row (floats): 16-B aligned, conflict-free
+// Chunk completion ring: the issuer commits chunk c's MMAs to done[c % NBF]; every role that
+// reuses a resource of chunk c (A stage, B stage, weight-ring bytes) waits on that phase.
+constexpr int NBF = 16;
+// PW mode (precomputed weight image): the weights of a schedule entry (nq in-reach blocks) are
+// nq x 2 KB of tf32 hi then nq x 2 KB of lo, already in the operand layout; one bulk copy per
+// entry into a byte ring in shared memory (entries placed contiguously, wrapping to 0).
+constexpr uint32_t SLOT_BYTES = TC_N * B_ROW;        // 2 KB: one block's 16 cells x 32 samples
+constexpr uint32_t RING = 76 * 1024;
+constexpr uint32_t REGION0 = RING > NBS * B_STAGE ? RING : NBS * B_STAGE;
 
 struct TcSmem {
-    uint8_t B[NBS][B_STAGE];
+    uint8_t B[REGION0];                   // OTF: NBS weight stages of B_STAGE; PW: the ring
     uint8_t Vs[NV][V_STAGE];
     float4 Gs[NV][TC_KC];                 // the chunk's sample geometry (plan order)
     uint4 Es[NV];                         // the chunk's schedule entry (written by the V loader)
-    uint32_t Bmask[NBS];                  // block mask of the chunk in each weight stage
-    // A stage s and B stage s hold the same chunk (NA == NBS): one commit frees both
-    uint64_t a_full[NA], b_full[NBS], s_empty[NA], v_full[NV], v_empty[NV];
+    uint32_t Bmask[NBF];                  // block mask of the chunk in each weight stage / ring entry
+    uint32_t Boff[NBF];                   // PW: ring offset of the entry
+    // A stage s and B stage s hold the same chunk (NA == NBS)
+    uint64_t a_full[NA], b_full[NBF], done[NBF], v_full[NV], v_empty[NV];
     uint64_t seg_done[2], seg_free[2];    // D buffer d: segment's MMAs complete / promoted
     uint64_t bar_done;
     uint32_t tmem_base;
@@ -119,12 +131,67 @@ struct TcSmem {
     alignas(16) float M[TC_M][T_LD];      // fp32 master sums [channel][cell] (padded rows)
 };
 
-static_assert(offsetof(TcSmem, B) == 0 && offsetof(TcSmem, Vs) == NBS * B_STAGE, "stage layout");
+static_assert(offsetof(TcSmem, B) == 0 && offsetof(TcSmem, Vs) % 1024 == 0, "stage layout");
+static_assert(sizeof(TcSmem) + 1024 <= 232448, "shared memory budget");
 
 // byte offset of (slot q, cell n, sample k) inside one half (hi or lo) of a B stage
 __device__ __forceinline__ uint32_t b_off(int q, int n, int kq) {
     const int r = q * TC_N + n;
     return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((kq ^ (r & 7)) << 4));
+}
+
+// The B operand of one chunk entry: thread wt (0..255) of the B-producer group computes its
+// (sample quad kq, column pair ch2, cell row rr) items of slots q0 = wt >> 6, q0 + 4 (slot q =
+// the entry's q-th in-reach block, blist order) and stores them, split into tf32 hi / lo, at
+// hi + b_off(q, n, kq) and lo + b_off(q, n, kq).  Used by the on-the-fly B producers (shared
+// memory) and by the plan's weight image (global memory): the bytes are identical.
+__device__ __forceinline__ void entry_weights(const Geom& g, const PlanDev& pd, int i0, int j0,
+                                              int wt, const float (&cosr)[TC_BY],
+                                              const float4 (&g4)[4], uint32_t pstart, int row,
+                                              uint32_t blist, int nq, uint8_t* hi, uint8_t* lo) {
+    const int kq = wt & 7, ch2 = (wt >> 3) & 1, rr = (wt >> 4) & 3, q0 = wt >> 6;
+#pragma unroll 1
+    for (int q = q0; q < nq; q += 4) {
+        const int b = (blist >> (4 * q)) & 15;
+        const int by = b / TC_BX;
+        const int cj = j0 + by * 4 + rr;
+        const int ci0 = i0 + (b % TC_BX) * 4;
+        float cos_c = cosr[0];
+#pragma unroll
+        for (int k = 1; k < TC_BY; ++k)
+            if (by == k) cos_c = cosr[k];
+        float w[4][2];                 // [sample][cell col]
+        patch_weights<2>(g, pd, row, cj, ci0, 2 * ch2, cos_c, g4, pstart + 4 * kq, w);
+        if (cj >= g.ny) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) w[u][cc] = 0.0f;
+        }
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+            const int n = rr * 4 + 2 * ch2 + cc;
+            uint4 h4, l4;
+            tc::split_tf32(w[0][cc], h4.x, l4.x);
+            tc::split_tf32(w[1][cc], h4.y, l4.y);
+            tc::split_tf32(w[2][cc], h4.z, l4.z);
+            tc::split_tf32(w[3][cc], h4.w, l4.w);
+            const uint32_t o = b_off(q, n, kq);
+            *reinterpret_cast<uint4*>(hi + o) = h4;
+            *reinterpret_cast<uint4*>(lo + o) = l4;
+        }
+    }
+}
+
+// cos(lat) of the cell rows a B-producer thread can touch (rr = its row within a block)
+__device__ __forceinline__ void entry_cos_rows(const Geom& g, const PlanDev& pd, int j0, int wt,
+                                               float (&cosr)[TC_BY]) {
+    const int rr = (wt >> 4) & 3;
+#pragma unroll
+    for (int by = 0; by < TC_BY; ++by) {
+        const int cj = j0 + by * 4 + rr;
+        cosr[by] = cj < g.ny ? __ldg(&pd.cos_row[cj]) : 1.0f;
+    }
 }
 
 // ------------------------------------------------------------------ plan-side pieces
@@ -273,6 +340,81 @@ __global__ void k_tc_wsum(const __grid_constant__ Geom g, PlanDev pd, float* __r
     wsum[cell] = W;
 }
 
+// The weight image (PW mode): one CTA of 256 threads per tile walks the tile's entries; the
+// threads compute the B-producer items of each entry (entry_weights) into global memory at
+// the entry's slots: [nq x 2 KB hi][nq x 2 KB lo], byte-identical to the shared-memory stage.
+__global__ void __launch_bounds__(W_THREADS)
+k_tc_wimage(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict__ sched,
+            const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ wslot,
+            uint8_t* __restrict__ wimg) {
+    const int tiles_x = (g.nx + TC_TW - 1) / TC_TW;
+    const int i0 = (blockIdx.x % tiles_x) * TC_TW, j0 = (blockIdx.x / tiles_x) * TC_TH;
+    const int wt = threadIdx.x, kq = wt & 7;
+    float cosr[TC_BY];
+    entry_cos_rows(g, pd, j0, wt, cosr);
+    for (uint32_t ei = tile_off[blockIdx.x]; ei < tile_off[blockIdx.x + 1]; ++ei) {
+        const uint4 e = __ldg(&sched[ei]);
+        const uint32_t pstart = e.x, nk = e.y & 63;
+        const int nq = __popc(e.z);
+        float4 g4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            g4[u] = (uint32_t)(4 * kq + u) < nk ? __ldg(&pd.geo[pstart + 4 * kq + u])
+                                                : make_float4(0.0f, kInvalidDy, 0.0f, 0.0f);
+        uint8_t* hi = wimg + (size_t)__ldg(&wslot[ei]) * (2u * SLOT_BYTES);
+        entry_weights(g, pd, i0, j0, wt, cosr, g4, pstart, (int)(e.y >> 6), e.w, nq, hi,
+                      hi + (size_t)nq * SLOT_BYTES);
+    }
+}
+
+// Build the weight image once per plan (first launch that asks for it).  Returns false (and
+// leaves the plan in on-the-fly mode) if the image does not fit the memory budget.
+static bool ensure_tc_wimage(const hegrid_plan_s* p, cudaStream_t st) {
+    if (p->tc_pw >= 0) return p->tc_pw == 1;
+    p->tc_pw = 0;
+    const Geom& g = p->g;
+    const int tiles = ((g.nx + TC_TW - 1) / TC_TW) * ((g.ny + TC_TH - 1) / TC_TH);
+    const int64_t ne = p->tc_nchunks;
+    if (ne <= 0) return false;
+    std::vector<uint4> h(ne);
+    if (cudaMemcpyAsync(h.data(), p->d_tc_sched, ne * sizeof(uint4), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return false;
+    std::vector<uint32_t> slot(ne);
+    uint64_t tot = 0;
+    for (int64_t i = 0; i < ne; ++i) {
+        slot[i] = (uint32_t)tot;
+        tot += (uint64_t)__builtin_popcount(h[i].z);
+    }
+    const uint64_t bytes = tot * 2u * SLOT_BYTES;
+    size_t fr = 0, total = 0;
+    if (tot >= (1ull << 32) || cudaMemGetInfo(&fr, &total) != cudaSuccess || bytes > fr / 4) return false;
+    uint8_t* d_img = nullptr;
+    uint32_t* d_slot = nullptr;
+    if (cudaMalloc(&d_img, bytes) != cudaSuccess) return false;
+    if (cudaMalloc(&d_slot, ne * sizeof(uint32_t)) != cudaSuccess) {
+        cudaFree(d_img);
+        return false;
+    }
+    cudaError_t e = cudaMemcpyAsync(d_slot, slot.data(), ne * sizeof(uint32_t), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+        k_tc_wimage<<<tiles, W_THREADS, 0, st>>>(g, p->dev(), p->d_tc_sched, p->d_tc_tile_off, d_slot, d_img);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        cudaFree(d_img);
+        cudaFree(d_slot);
+        return false;
+    }
+    p->d_tc_wimg = d_img;
+    p->d_tc_wslot = d_slot;
+    p->tc_wimg_bytes = (int64_t)bytes;
+    p->tc_pw = 1;
+    return true;
+}
+
 static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     if (p->tc_nchunks >= 0) return HEGRID_OK;
     const Geom& g = p->g;
@@ -342,11 +484,12 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
 __device__ unsigned long long g_tc_prof[16];
 
 // ------------------------------------------------------------------ the kernel
-template <int SEG>
+template <int SEG, bool PW>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap tmap_v,
            PlanDev pd, const uint4* __restrict__ sched,
            const uint32_t* __restrict__ tile_off, const float* __restrict__ wsum,
+           const uint8_t* __restrict__ wimg, const uint32_t* __restrict__ wslot,
            int C, float* __restrict__ out, float* __restrict__ wout, int dbg_in) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_raw);
@@ -374,16 +517,14 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 
     if (warp == 0) tc::tmem_alloc(&sm.tmem_base, TMEM_COLS);
     if (tid == 32) {
-        for (int s = 0; s < NA; ++s) {
-            tc::mbar_init(&sm.a_full[s], 128);
-            tc::mbar_init(&sm.s_empty[s], 1);
-        }
-        for (int s = 0; s < NBS; ++s) {
-            tc::mbar_init(&sm.b_full[s], W_THREADS);
+        for (int s = 0; s < NA; ++s) tc::mbar_init(&sm.a_full[s], 128);
+        for (int s = 0; s < NBF; ++s) {
+            tc::mbar_init(&sm.done[s], 1);
+            tc::mbar_init(&sm.b_full[s], PW ? 1 : W_THREADS);   // PW: the weight loader's tx
         }
         for (int s = 0; s < NV; ++s) {
             tc::mbar_init(&sm.v_full[s], 1);
-            tc::mbar_init(&sm.v_empty[s], 128 + W_THREADS);
+            tc::mbar_init(&sm.v_empty[s], PW ? 128 : 128 + W_THREADS);
         }
         for (int d = 0; d < 2; ++d) {
             tc::mbar_init(&sm.seg_done[d], 1);
@@ -464,7 +605,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     tc::fence_after_sync();
                 }
             }
-            const int sa = c % NA, sb = c % NBS;
+            const int sa = c % NA, sb = PW ? c % NBF : c % NBS;
             {
                 TPROF_BEGIN;
                 tc::mbar_wait(&sm.a_full[sa], (c / NA) & 1);
@@ -472,17 +613,21 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             }
             {
                 TPROF_BEGIN;
-                tc::mbar_wait(&sm.b_full[sb], (c / NBS) & 1);
+                tc::mbar_wait(&sm.b_full[sb], PW ? (c / NBF) & 1 : (c / NBS) & 1);
                 TPROF_END(1);
             }
             tc::fence_after_sync();
             const uint32_t mask = sm.Bmask[sb];
+            // B operand: OTF = weight stage sb (lo half at B_HALF); PW = the entry's ring bytes
+            // (nq slots of hi, then nq slots of lo)
+            const uint32_t b_addr = PW ? tc::smem_u32(&sm.B[sm.Boff[sb]]) : tc::smem_u32(&sm.B[sb * B_STAGE]);
+            const uint64_t lo16 = PW ? (uint64_t)((__popc(mask) * SLOT_BYTES) >> 4) : (uint64_t)(B_HALF >> 4);
             TPROF_BEGIN;
             if (!(dbg & 2)) {
                 // runs of consecutive in-reach blocks = consecutive B slots (slots follow the
                 // mask order); D buffers are zeroed before each segment, so every MMA
                 // accumulates.  Each run is 12 MMAs behind one elect.
-                const uint64_t dh0 = tc::sdesc_sw128(tc::smem_u32(&sm.B[sb][0]));
+                const uint64_t dh0 = tc::sdesc_sw128(b_addr);
                 const uint32_t a0 = tmem + A_COL0 + sa * 64;
                 const uint32_t dbase = tmem + (uint32_t)d * D_COLS;
                 uint32_t mm = mask;
@@ -491,13 +636,13 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     const int b = __ffs(mm) - 1;
                     const int r = __ffs(~(mm >> b)) - 1;
                     mm &= ~(((1u << r) - 1u) << b);
-                    tc::mma_run_3xtf32<(32 >> 4), (B_HALF >> 4)>(
-                        dbase + (uint32_t)(b * TC_N), a0, dh0 + (uint64_t)((q * TC_N * B_ROW) >> 4),
+                    tc::mma_run_3xtf32<(32 >> 4)>(
+                        dbase + (uint32_t)(b * TC_N), a0, dh0 + (uint64_t)((q * SLOT_BYTES) >> 4), lo16,
                         tc::idesc_tf32(TC_M, TC_N * r), 1u);
                     q += r;
                 }
             }
-            tc::mma_commit_warp(&sm.s_empty[sa]);      // a commit costs ~100 cycles: one per chunk
+            tc::mma_commit_warp(&sm.done[c % NBF]);    // a commit costs ~100 cycles: one per chunk
             if (c % SEG == SEG - 1 || c == nchunks - 1) tc::mma_commit_warp(&sm.seg_done[d]);
             __syncwarp();
             TPROF_END(2);
@@ -541,13 +686,50 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 if (dbg & 8) {
                     tc::mbar_arrive(&sm.v_full[sv]);
                 } else {
-                    tc::mbar_arrive_expect_tx(&sm.v_full[sv], (uint32_t)V_STAGE + nk * 16);
+                    // the geometry feeds the on-the-fly B producers only
+                    tc::mbar_arrive_expect_tx(&sm.v_full[sv], (uint32_t)V_STAGE + (PW ? 0u : nk * 16));
                     tc::tma_load_2d(&sm.Vs[sv][0], &tmap_v, cb, (int)e.x, &sm.v_full[sv]);
-                    tc::bulk_g2s(&sm.Gs[sv][0], pd.geo + e.x, nk * 16, &sm.v_full[sv]);
+                    if (!PW) tc::bulk_g2s(&sm.Gs[sv][0], pd.geo + e.x, nk * 16, &sm.v_full[sv]);
                 }
             }
             __syncwarp();
         }
+    } else if (PW && warp == 2) {
+        // ============================ weight loader (PW) ======================
+        // entry c's nq x 4 KB of precomputed weights -> the ring at the next contiguous offset
+        // (wrapping to 0); the bytes are reused once every chunk placed there has completed
+        // (done[] phases, confirmed in order).  At most NBF entries are in flight.
+        if (lane == 0) {
+            const uint32_t* ws = wslot + tile_off[blockIdx.x];
+            long long head = 0, starts[NBF];
+            int conf = 0;                         // chunks confirmed complete
+            for (int c = 0; c < nchunks; ++c) {
+                const uint4 e = __ldg(&cs[c]);
+                const uint32_t nq = __popc(e.z), bytes = nq * 2u * SLOT_BYTES;
+                long long off = head % RING;
+                if (off + bytes > RING) {
+                    head += RING - off;
+                    off = 0;
+                }
+                TPROF_BEGIN;
+                // reuse: the slot barrier of chunk c - NBF, and every chunk that started less than
+                // one ring length before this entry's end
+                while (conf < c && (c - conf >= NBF || starts[conf % NBF] < head + (long long)bytes - RING)) {
+                    tc::mbar_wait(&sm.done[conf % NBF], (conf / NBF) & 1);
+                    ++conf;
+                }
+                TPROF_END(0);
+                starts[c % NBF] = head;
+                const int k = c % NBF;
+                sm.Bmask[k] = e.z;
+                sm.Boff[k] = (uint32_t)off;
+                tc::fence_after_sync();
+                tc::mbar_arrive_expect_tx(&sm.b_full[k], bytes);
+                tc::bulk_g2s(&sm.B[off], wimg + (size_t)__ldg(&ws[c]) * (2u * SLOT_BYTES), bytes, &sm.b_full[k]);
+                head += bytes;
+            }
+        }
+        __syncwarp();
     }
     // A producers keep the block masks of the (at most two) segments not yet promoted
     uint32_t segmask0 = 0u, segmask1 = 0u;   // (scalars: no local-memory array)
@@ -586,7 +768,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const int sa = c % NA;
             {
                 TPROF_BEGIN;
-                if (c >= NA) tc::mbar_wait(&sm.s_empty[sa], ((c / NA) - 1) & 1);
+                if (c >= NA) tc::mbar_wait(&sm.done[(c - NA) % NBF], ((c - NA) / NBF) & 1);
                 TPROF_END(1);
             }
             tc::fence_after_sync();
@@ -628,19 +810,14 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 store(cn);
             }
         }
-    } else if (warp >= 8) {
+    } else if (!PW && warp >= 8) {
         // ============================ B producers ============================
-        // item = (slot q, cell row rr, column pair ch2, sample quad kq): 4 samples x 2 cells;
-        // a thread keeps (kq, ch2, rr) and takes slots q0 and q0 + 4 (64 items per slot, so
-        // every B warp has work as soon as the chunk reaches 4 blocks)
+        // (on-the-fly mode only) item = (slot q, cell row rr, column pair ch2, sample quad
+        // kq): 4 samples x 2 cells; a thread keeps (kq, ch2, rr) and takes slots q0, q0 + 4
         const int wt = tid - 8 * 32;                  // 0..255
-        const int kq = wt & 7, ch2 = (wt >> 3) & 1, rr = (wt >> 4) & 3, q0 = wt >> 6;
-        float cosr[TC_BY];                        // cos(lat) of this thread's possible rows
-#pragma unroll
-        for (int by = 0; by < TC_BY; ++by) {
-            const int cj = j0 + by * 4 + rr;
-            cosr[by] = cj < g.ny ? __ldg(&pd.cos_row[cj]) : 1.0f;
-        }
+        const int kq = wt & 7;
+        float cosr[TC_BY];
+        entry_cos_rows(g, pd, j0, wt, cosr);
         for (int c = 0; c < nchunks; ++c) {
             const int sv = c % NV;
             float4 g4[4];
@@ -673,52 +850,13 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const int sb = c % NBS;
             {
                 TPROF_BEGIN;
-                if (c >= NBS) tc::mbar_wait(&sm.s_empty[sb], ((c / NBS) - 1) & 1);
+                if (c >= NBS) tc::mbar_wait(&sm.done[(c - NBS) % NBF], ((c - NBS) / NBF) & 1);
                 TPROF_END(0);
             }
             TPROF_BEGIN;
-            // slot q holds the q-th in-reach block of the entry (mask order, blist)
             const int nq = (dbg & 1) ? 0 : __popc(mask);
-            uint8_t* bst = &sm.B[sb][0];
-#pragma unroll 1
-            for (int q = q0; q < nq; q += 4) {
-                const int b = (blist >> (4 * q)) & 15;
-                const int by = b / TC_BX;
-                const int cj = j0 + by * 4 + rr;
-                const int ci0 = i0 + (b % TC_BX) * 4;
-                const bool rok = cj < g.ny;
-                float cos_c = cosr[0];
-#pragma unroll
-                for (int k = 1; k < TC_BY; ++k)
-                    if (by == k) cos_c = cosr[k];
-                float w[4][2];                 // [sample][cell col]
-                if (dbg & 64) {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-#pragma unroll
-                        for (int cc = 0; cc < 2; ++cc) w[u][cc] = g4[u].x * cos_c + (float)cc;
-                } else {
-                    patch_weights<2>(g, pd, row, cj, ci0, 2 * ch2, cos_c, g4, pstart + 4 * kq, w);
-                    if (!rok) {
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-#pragma unroll
-                            for (int cc = 0; cc < 2; ++cc) w[u][cc] = 0.0f;
-                    }
-                }
-#pragma unroll
-                for (int cc = 0; cc < 2; ++cc) {
-                    const int n = rr * 4 + 2 * ch2 + cc;
-                    uint4 h4, l4;
-                    tc::split_tf32(w[0][cc], h4.x, l4.x);
-                    tc::split_tf32(w[1][cc], h4.y, l4.y);
-                    tc::split_tf32(w[2][cc], h4.z, l4.z);
-                    tc::split_tf32(w[3][cc], h4.w, l4.w);
-                    const uint32_t o = b_off(q, n, kq);
-                    *reinterpret_cast<uint4*>(bst + o) = h4;
-                    *reinterpret_cast<uint4*>(bst + B_HALF + o) = l4;
-                }
-            }
+            uint8_t* bst = &sm.B[sb * B_STAGE];
+            entry_weights(g, pd, i0, j0, wt, cosr, g4, pstart, row, blist, nq, bst, bst + B_HALF);
             if (wt == 0) sm.Bmask[sb] = mask;
             if (!(dbg & 128)) tc::fence_proxy_async_smem();
             tc::mbar_arrive(&sm.b_full[sb]);
@@ -825,10 +963,17 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     if (const char* e = getenv("HEGRID_TC_DEBUG")) dbg = atoi(e);
     const bool sparse = p->tc_max_cpb <= TC_CPB_SPARSE;
     const int SEG = sparse ? SEG_SPARSE : SEG_DENSE;
-    auto kern = sparse ? k_accum_tc<SEG_SPARSE> : k_accum_tc<SEG_DENSE>;
+    // Precomputed weights pay once several channel blocks share them (each block would
+    // otherwise recompute every weight); HEGRID_TC_PW=0/1 forces the choice.
+    int want_pw = grid.y >= TC_PW_MIN_CBLOCKS;
+    if (const char* e = getenv("HEGRID_TC_PW")) want_pw = atoi(e);
+    const bool pw = want_pw && ensure_tc_wimage(p, st);
+    auto kern = pw ? (sparse ? k_accum_tc<SEG_SPARSE, true> : k_accum_tc<SEG_DENSE, true>)
+                   : (sparse ? k_accum_tc<SEG_SPARSE, false> : k_accum_tc<SEG_DENSE, false>);
     HG_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched, p->d_tc_tile_off,
-                                         p->d_tc_wsum, C, d_out, d_weight, dbg);
+                                         p->d_tc_wsum, p->d_tc_wimg, p->d_tc_wslot, C, d_out,
+                                         d_weight, dbg);
     count_launch();
     if (dbg & 32) {
         unsigned long long h[16];

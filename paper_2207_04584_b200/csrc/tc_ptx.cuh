@@ -125,16 +125,16 @@ __device__ __forceinline__ void mma_tf32_ts_warp_acc(uint32_t d_tmem, uint32_t a
 }
 // One run of the 3xTF32 product over a 32-sample chunk: 4 K-steps x (hi*hi, hi*lo, lo*hi),
 // 12 MMAs behind a single elect.  A stage in TMEM: hi at columns a0 + 8 ks, lo at
-// a0 + 32 + 8 ks; B descriptors: hi at b0 + ks * KS_STEP (16-B units), lo at + LO_OFF.
+// a0 + 32 + 8 ks; B descriptors: hi at b0 + ks * KS_STEP (16-B units), lo at + lo_off.
 // The first MMA accumulates iff acc0 != 0, the other 11 always accumulate.
-template <int KS_STEP, int LO_OFF>
+template <int KS_STEP>
 __device__ __forceinline__ void mma_run_3xtf32(uint32_t d, uint32_t a0, uint64_t b0,
-                                               uint32_t idesc, uint32_t acc0) {
-#define HG_MMA_KS(ka, kl, bo, blo)                                                         \
+                                               uint64_t lo_off, uint32_t idesc, uint32_t acc0) {
+#define HG_MMA_KS(ka, kl, bo)                                                              \
     "add.u32 ah, %1, " #ka ";\n\t"                                                         \
     "add.u32 al, %1, " #kl ";\n\t"                                                         \
     "add.s64 bh, %2, %" #bo ";\n\t"                                                        \
-    "add.s64 bl, %2, %" #blo ";\n\t"                                                       \
+    "add.s64 bl, bh, %5;\n\t"                                                              \
     "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bh, %3, t;\n\t"                    \
     "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bl, %3, t;\n\t"                    \
     "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], bh, %3, t;\n\t"
@@ -151,10 +151,9 @@ __device__ __forceinline__ void mma_run_3xtf32(uint32_t d, uint32_t a0, uint64_t
         "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], bl, %3, t;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], %2, %3, t;\n\t"
-        HG_MMA_KS(8, 40, 6, 7) HG_MMA_KS(16, 48, 8, 9) HG_MMA_KS(24, 56, 10, 11)
-        "}\n" :: "r"(d), "r"(a0), "l"(b0), "r"(idesc), "r"(acc0),
-        "n"(LO_OFF), "n"(KS_STEP), "n"(KS_STEP + LO_OFF), "n"(2 * KS_STEP),
-        "n"(2 * KS_STEP + LO_OFF), "n"(3 * KS_STEP), "n"(3 * KS_STEP + LO_OFF));
+        HG_MMA_KS(8, 40, 6) HG_MMA_KS(16, 48, 7) HG_MMA_KS(24, 56, 8)
+        "}\n" :: "r"(d), "r"(a0), "l"(b0), "r"(idesc), "r"(acc0), "l"(lo_off),
+        "n"(KS_STEP), "n"(2 * KS_STEP), "n"(3 * KS_STEP));
 #undef HG_MMA_KS
 }
 __device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {

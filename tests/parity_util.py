@@ -61,3 +61,12 @@ def plan_layout_values(w, lon, lat, perm, channels, ld=None, device="cuda"):
         blk = synth.values(w, lon_d, lat_d, channels=ch, samples=perm_t)  # [cb][n_used]
         out[:, c0:c0 + ch.shape[0]] = blk.t()
     return out
+
+
+def engine_env(engine, monkeypatch):
+    """Test engine names -> Plan engine.  "tc_pw" / "tc_otf" force the tensor-core engine's
+    precomputed-weight image on / off (HEGRID_TC_PW); "tc" leaves the library's choice."""
+    if engine in ("tc_pw", "tc_otf"):
+        monkeypatch.setenv("HEGRID_TC_PW", "1" if engine == "tc_pw" else "0")
+        return "tc"
+    return engine

@@ -9,7 +9,7 @@ import torch
 import oracle
 import synth
 from paper_2207_04584_b200 import Plan
-from parity_util import RTOL, plan_layout_values
+from parity_util import RTOL, engine_env, plan_layout_values
 
 pytestmark = pytest.mark.gpu
 
@@ -26,10 +26,11 @@ def sample_channels(C, k=12):
     return np.array(ch, np.int64)
 
 
-@pytest.mark.parametrize("engine", ["simt", "tc"])
+@pytest.mark.parametrize("engine", ["simt", "tc_otf", "tc_pw"])
 @pytest.mark.parametrize("name,channels", [("cfg2", None), ("cfg3", None), ("cfg4", None),
                                            ("cfg5", 260)])
-def test_fullsize_sampled_parity(name, channels, engine):
+def test_fullsize_sampled_parity(name, channels, engine, monkeypatch):
+    engine = engine_env(engine, monkeypatch)
     w = synth.CONFIGS[name]
     C = w.channels if channels is None else channels
     lon, lat = synth.coords(w, device="cuda")

@@ -14,11 +14,11 @@ import torch
 import oracle
 import synth
 from paper_2207_04584_b200 import Plan, _binding as b
-from parity_util import compare, make_inputs, oracle_grid, plan_layout_values, small_workload
+from parity_util import compare, engine_env, make_inputs, oracle_grid, plan_layout_values, small_workload
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = ["simt", "tc"]
+ENGINES = ["simt", "tc", "tc_pw"]
 
 
 # ------------------------------------------------------------------ plan layer
@@ -87,7 +87,8 @@ def test_plan_permutation_is_stable_bin_order_cfg2_small():
 
 # ------------------------------------------------------------------ Eq. 1 parity
 @pytest.mark.parametrize("engine", ENGINES)
-def test_grid_cfg1_full_parity(engine):
+def test_grid_cfg1_full_parity(engine, monkeypatch):
+    engine = engine_env(engine, monkeypatch)
     """BASELINE configs[0] in full: 5000 samples, 64x64, 1 channel."""
     w, lon, lat, vals = _cfg1()
     with Plan(lon, lat, w.map, w.fwhm_deg, engine=engine) as p:
@@ -98,7 +99,8 @@ def test_grid_cfg1_full_parity(engine):
 
 
 @pytest.mark.parametrize("engine", ENGINES)
-def test_grid_drift_scan_many_channels_ragged(engine):
+def test_grid_drift_scan_many_channels_ragged(engine, monkeypatch):
+    engine = engine_env(engine, monkeypatch)
     """cfg2-shaped drift scan at oracle-friendly size: 70x61 map (ragged tiles), 133
     channels (two 128-channel blocks, ragged tail)."""
     w = small_workload("cfg2", n=220 * 180, tracks=220, per_track=180, nx=70, ny=61,
@@ -111,7 +113,8 @@ def test_grid_drift_scan_many_channels_ragged(engine):
 
 
 @pytest.mark.parametrize("engine", ENGINES)
-def test_grid_high_density_cfg3_shape(engine):
+def test_grid_high_density_cfg3_shape(engine, monkeypatch):
+    engine = engine_env(engine, monkeypatch)
     """cfg3's density (1e6 samples/deg^2) and kernel (FWHM 6.925', ~84k neighbours per
     cell) on a 0.4 deg field, 24x24 map, 7 channels."""
     w = small_workload("cfg3", n=160_000, field_lon=0.4, field_lat=0.4, nx=24, ny=24,
@@ -126,7 +129,8 @@ def test_grid_high_density_cfg3_shape(engine):
 
 
 @pytest.mark.parametrize("engine", ENGINES)
-def test_device_paths_bit_identical_and_deterministic(engine):
+def test_device_paths_bit_identical_and_deterministic(engine, monkeypatch):
+    engine = engine_env(engine, monkeypatch)
     """Host path, device USER_CN path and device PLAN_NC path give bit-identical maps;
     repeated runs are bit-identical (no atomics, fixed summation order)."""
     w = small_workload("cfg2", n=120 * 100, tracks=120, per_track=100, nx=40, ny=37,
@@ -185,7 +189,8 @@ def mk_map(nx, ny, lon0, lat0, dl, dlat=None):
 
 
 @pytest.mark.parametrize("engine", ENGINES)
-def test_empty_input_all_blank(engine):
+def test_empty_input_all_blank(engine, monkeypatch):
+    engine = engine_env(engine, monkeypatch)
     m = mk_map(9, 7, 30, 41, 1 / 60)
     with Plan(np.zeros(0), np.zeros(0), m, 0.05, engine=engine) as p:
         out, W = p.grid(np.zeros((3, 0), np.float32))
@@ -193,7 +198,8 @@ def test_empty_input_all_blank(engine):
 
 
 @pytest.mark.parametrize("engine", ENGINES)
-def test_zero_channels_writes_weight_map(engine):
+def test_zero_channels_writes_weight_map(engine, monkeypatch):
+    engine = engine_env(engine, monkeypatch)
     rng = np.random.default_rng(0)
     lon = 30 + rng.uniform(-0.1, 0.1, 500)
     lat = 41 + rng.uniform(-0.1, 0.1, 500)
@@ -205,7 +211,8 @@ def test_zero_channels_writes_weight_map(engine):
 
 
 @pytest.mark.parametrize("engine", ENGINES)
-def test_sample_at_cell_centre_weight_one_and_outside_samples_dropped(engine):
+def test_sample_at_cell_centre_weight_one_and_outside_samples_dropped(engine, monkeypatch):
+    engine = engine_env(engine, monkeypatch)
     m = mk_map(16, 16, 30, 41, 1 / 60)
     lon_c, lat_c = oracle.cell_centre(m, 5, 9)
     lon = np.array([lon_c, 31.5, 28.0, lon_c])
@@ -217,7 +224,8 @@ def test_sample_at_cell_centre_weight_one_and_outside_samples_dropped(engine):
 
 
 @pytest.mark.parametrize("engine", ENGINES)
-def test_negative_cdelt_and_lon_zero_straddle(engine):
+def test_negative_cdelt_and_lon_zero_straddle(engine, monkeypatch):
+    engine = engine_env(engine, monkeypatch)
     rng = np.random.default_rng(4)
     lon = (rng.uniform(-0.25, 0.25, 6000) + 360.0) % 360.0
     lat = rng.uniform(-0.2, 0.2, 6000)
