@@ -37,6 +37,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <type_traits>
 #include <vector>
 
 #include <cuda.h>
@@ -593,7 +594,11 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 
     if (warp == 0) {
         // ============================ MMA issuer =============================
-        for (int c = 0; c < nchunks; ++c) {
+        // chunk c uses A stage c % NA; the loop is unrolled by NA so the stage (and with it
+        // every A operand address) is a compile-time constant in each body
+        static_assert(NA == 2, "issuer unrolled for two A stages");
+        auto issue = [&](const int c, auto SA_) {
+            constexpr int sa = decltype(SA_)::value;
             const int seg = c / SEG, d = seg & 1;
             if (c % SEG == 0) {
                 // a new segment accumulates into D buffer d, which the A warps have promoted
@@ -605,7 +610,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     tc::fence_after_sync();
                 }
             }
-            const int sa = c % NA, sb = PW ? c % NBF : c % NBS;
+            const int sb = PW ? c % NBF : c % NBS;
             {
                 TPROF_BEGIN;
                 tc::mbar_wait(&sm.a_full[sa], (c / NA) & 1);
@@ -627,7 +632,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 // runs of consecutive in-reach blocks = consecutive B slots (slots follow the
                 // mask order); D buffers are zeroed before each segment, so every MMA
                 // accumulates.  Each run is 12 MMAs behind one elect.
-                const uint64_t dh0 = tc::sdesc_sw128(b_addr);
+                const uint32_t dh0 = tc::sdesc_sw128_lo(b_addr);
                 const uint32_t a0 = tmem + A_COL0 + sa * 64;
                 const uint32_t dbase = tmem + (uint32_t)d * D_COLS;
                 uint32_t mm = mask;
@@ -636,9 +641,9 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     const int b = __ffs(mm) - 1;
                     const int r = __ffs(~(mm >> b)) - 1;
                     mm &= ~(((1u << r) - 1u) << b);
-                    tc::mma_run_3xtf32<(32 >> 4)>(
-                        dbase + (uint32_t)(b * TC_N), a0, dh0 + (uint64_t)((q * SLOT_BYTES) >> 4), lo16,
-                        tc::idesc_tf32(TC_M, TC_N * r), 1u);
+                    const uint32_t bh = dh0 + (uint32_t)((q * SLOT_BYTES) >> 4);
+                    tc::mma12_3xtf32<(32 >> 4)>(dbase + (uint32_t)(b * TC_N), a0, bh, bh + (uint32_t)lo16,
+                                                tc::idesc_tf32(TC_M, TC_N * r));
                     q += r;
                 }
             }
@@ -646,7 +651,13 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             if (c % SEG == SEG - 1 || c == nchunks - 1) tc::mma_commit_warp(&sm.seg_done[d]);
             __syncwarp();
             TPROF_END(2);
+        };
+        int c = 0;
+        for (; c + 1 < nchunks; c += 2) {
+            issue(c, std::integral_constant<int, 0>{});
+            issue(c + 1, std::integral_constant<int, 1>{});
         }
+        if (c < nchunks) issue(c, std::integral_constant<int, 0>{});
         tc::mma_commit_warp(&sm.bar_done);
         __syncwarp();
     } else if (warp == 1) {

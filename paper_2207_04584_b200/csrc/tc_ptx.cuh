@@ -156,6 +156,50 @@ __device__ __forceinline__ void mma_run_3xtf32(uint32_t d, uint32_t a0, uint64_t
         "n"(KS_STEP), "n"(2 * KS_STEP), "n"(3 * KS_STEP));
 #undef HG_MMA_KS
 }
+// The same 12 MMAs issued so that ptxas keeps the operand arithmetic in uniform registers:
+// TMEM operands as [base + immediate] (A hi at a0 + 8 ks, lo at a0 + 32 + 8 ks) and the B
+// descriptors built inside the asm from their low words (start address, LBO) with the
+// constant high word of a K-major SWIZZLE_128B descriptor (SBO = 1024 B, version 1), the
+// K-step advancing the start address by KS_STEP (16-B units).  Each base value is moved to a
+// uniform register once per run instead of once per MMA.
+constexpr uint32_t kDescHiSw128 = 0x40004040u;   // layout 2 << 61 | version << 46 | (1024 >> 4) << 32
+template <int KS_STEP>
+__device__ __forceinline__ void mma12_3xtf32(uint32_t d, uint32_t a0, uint32_t bh_lo, uint32_t bl_lo,
+                                             uint32_t idesc) {
+#define HG_MMA12_KS(ks, bh, bl, ah, al)                                                  \
+    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+" #ah "], " #bh ", %4, 1;\n\t"       \
+    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+" #ah "], " #bl ", %4, 1;\n\t"       \
+    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+" #al "], " #bh ", %4, 1;\n\t"
+    asm volatile(
+        "{\n\t"
+        ".reg .pred e;\n\t"
+        ".reg .b32 x1, x2, x3, y1, y2, y3;\n\t"
+        ".reg .b64 h0, h1, h2, h3, l0, l1, l2, l3;\n\t"
+        "add.u32 x1, %2, %5;\n\t"
+        "add.u32 x2, %2, %6;\n\t"
+        "add.u32 x3, %2, %7;\n\t"
+        "add.u32 y1, %3, %5;\n\t"
+        "add.u32 y2, %3, %6;\n\t"
+        "add.u32 y3, %3, %7;\n\t"
+        "mov.b64 h0, {%2, %8};\n\t"
+        "mov.b64 h1, {x1, %8};\n\t"
+        "mov.b64 h2, {x2, %8};\n\t"
+        "mov.b64 h3, {x3, %8};\n\t"
+        "mov.b64 l0, {%3, %8};\n\t"
+        "mov.b64 l1, {y1, %8};\n\t"
+        "mov.b64 l2, {y2, %8};\n\t"
+        "mov.b64 l3, {y3, %8};\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        HG_MMA12_KS(0, h0, l0, 0, 32) HG_MMA12_KS(1, h1, l1, 8, 40)
+        HG_MMA12_KS(2, h2, l2, 16, 48) HG_MMA12_KS(3, h3, l3, 24, 56)
+        "}\n" :: "r"(d), "r"(a0), "r"(bh_lo), "r"(bl_lo), "r"(idesc), "n"(KS_STEP),
+        "n"(2 * KS_STEP), "n"(3 * KS_STEP), "n"(kDescHiSw128) : "memory");
+#undef HG_MMA12_KS
+}
+// low word of a K-major SWIZZLE_128B descriptor (start address >> 4, LBO field 1)
+__device__ __forceinline__ uint32_t sdesc_sw128_lo(uint32_t saddr) {
+    return ((saddr >> 4) & 0x3FFFu) | (1u << 16);
+}
 __device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
     asm volatile(
         "{\n\t"

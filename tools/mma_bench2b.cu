@@ -26,7 +26,7 @@ __global__ void k_bench(int r, int runs_per_chunk, int chunks, int st_interfere,
         for (int c = 0; c < chunks; ++c) {
             const uint32_t a0 = t + 256 + (c & 3) * 64;
             for (int k = 0; k < runs_per_chunk; ++k)
-                tc::mma_run_3xtf32<2>(t + (uint32_t)(k * 16 * r) % 64u, a0, d0 + (uint64_t)(k * r * 128), 1024, idesc, 1);
+                tc::mma12_3xtf32<2>(t + (uint32_t)(k * 16 * r) % 64u, a0, d0 + (uint64_t)(k * r * 128), d0 + 1024 + (uint64_t)(k * r * 128), idesc);
             for (int k = 0; k < commits; ++k) tc::mma_commit_warp(&cb[k]);
         }
         long long t1 = clock64();
@@ -51,9 +51,9 @@ int main() {
     unsigned long long* d;
     cudaMalloc(&d, 16);
     cudaFuncSetAttribute(k_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    for (int cm : {1}) {
+    for (int cm : {0, 1}) {
         for (int r : {1, 2, 3, 4, 6, 8, 12}) {
-            int chunks = 256, rpc = 1, st = 0;
+            int chunks = 256, rpc = 2, st = 0;
             k_bench<<<148, 256, 64 * 1024>>>(r, rpc, chunks, st, cm, d);
             cudaError_t e = cudaDeviceSynchronize();
             unsigned long long h[2];
