@@ -491,7 +491,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
            PlanDev pd, const uint4* __restrict__ sched,
            const uint32_t* __restrict__ tile_off, const float* __restrict__ wsum,
            const uint8_t* __restrict__ wimg, const uint32_t* __restrict__ wslot,
-           int C, float* __restrict__ out, float* __restrict__ wout, int dbg_in) {
+           int C, int tiles, int cgroup, float* __restrict__ out, float* __restrict__ wout,
+           int dbg_in) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_raw);
     if (tc::smem_u32(smem_raw) & 1023u) __trap();   // swizzle atoms need 1024-B alignment
@@ -510,10 +511,20 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 #define TPROF_BEGIN long long _t0 = prof ? clock64() : 0
 #define TPROF_END(k) if (prof) pw[k] += (unsigned long long)(clock64() - _t0)
     const int tiles_x = (g.nx + TC_TW - 1) / TC_TW;
-    const int i0 = (blockIdx.x % tiles_x) * TC_TW, j0 = (blockIdx.x / tiles_x) * TC_TH;
-    const int cb = blockIdx.y * TC_M;
-    const uint4* cs = sched + tile_off[blockIdx.x];
-    const int nchunks = (int)(tile_off[blockIdx.x + 1] - tile_off[blockIdx.x]);
+    // CTA -> (tile, channel block): channel blocks in groups of `cgroup`, the group's blocks
+    // fastest, so the CTAs resident together share their tiles' weight entries in L2
+    int tile, cblk;
+    {
+        const int ncb = (C + TC_M - 1) / TC_M;
+        const int lin = blockIdx.x, grp = lin / (tiles * cgroup), within = lin % (tiles * cgroup);
+        const int gsz = min(cgroup, ncb - grp * cgroup);
+        tile = within / gsz;
+        cblk = grp * cgroup + within % gsz;
+    }
+    const int i0 = (tile % tiles_x) * TC_TW, j0 = (tile / tiles_x) * TC_TH;
+    const int cb = cblk * TC_M;
+    const uint4* cs = sched + tile_off[tile];
+    const int nchunks = (int)(tile_off[tile + 1] - tile_off[tile]);
     const int64_t cells = (int64_t)g.nx * g.ny;
 
     if (warp == 0) tc::tmem_alloc(&sm.tmem_base, TMEM_COLS);
@@ -711,12 +722,18 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         // (wrapping to 0); the bytes are reused once every chunk placed there has completed
         // (done[] phases, confirmed in order).  At most NBF entries are in flight.
         if (lane == 0) {
-            const uint32_t* ws = wslot + tile_off[blockIdx.x];
+            const uint32_t* ws = wslot + tile_off[tile];
             long long head = 0, starts[NBF];
             int conf = 0;                         // chunks confirmed complete
+            constexpr int WPF = 8;                // L2 prefetch distance (entries)
+            for (int c = 0; c < WPF && c < nchunks; ++c)
+                tc::prefetch_l2(wimg + (size_t)__ldg(&ws[c]) * (2u * SLOT_BYTES), __popc(__ldg(&cs[c].z)) * 2u * SLOT_BYTES);
             for (int c = 0; c < nchunks; ++c) {
                 const uint4 e = __ldg(&cs[c]);
                 const uint32_t nq = __popc(e.z), bytes = nq * 2u * SLOT_BYTES;
+                if (c + WPF < nchunks)
+                    tc::prefetch_l2(wimg + (size_t)__ldg(&ws[c + WPF]) * (2u * SLOT_BYTES),
+                                    __popc(__ldg(&cs[c + WPF].z)) * 2u * SLOT_BYTES);
                 long long off = head % RING;
                 if (off + bytes > RING) {
                     head += RING - off;
@@ -900,7 +917,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             }
         }
     }
-    if (blockIdx.y == 0 && wout != nullptr && tid < TC_TW * TC_TH) {
+    if (cblk == 0 && wout != nullptr && tid < TC_TW * TC_TH) {
         const int i = i0 + tid % TC_TW, j = j0 + tid / TC_TW;
         if (i < g.nx && j < g.ny) wout[(int64_t)j * g.nx + i] = __ldg(&wsum[(int64_t)j * g.nx + i]);
     }
@@ -968,7 +985,8 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     const Geom& g = p->g;
     int C = (int)n_channels;
     int tiles = ((g.nx + TC_TW - 1) / TC_TW) * ((g.ny + TC_TH - 1) / TC_TH);
-    dim3 grid(tiles, (C + TC_M - 1) / TC_M);
+    const int ncb = (C + TC_M - 1) / TC_M;
+    dim3 grid(tiles * ncb);
     size_t smem = sizeof(TcSmem);
     int dbg = 0;
     if (const char* e = getenv("HEGRID_TC_DEBUG")) dbg = atoi(e);
@@ -976,15 +994,20 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     const int SEG = sparse ? SEG_SPARSE : SEG_DENSE;
     // Precomputed weights pay once several channel blocks share them (each block would
     // otherwise recompute every weight); HEGRID_TC_PW=0/1 forces the choice.
-    int want_pw = grid.y >= TC_PW_MIN_CBLOCKS;
+    int want_pw = ncb >= (int)TC_PW_MIN_CBLOCKS;
     if (const char* e = getenv("HEGRID_TC_PW")) want_pw = atoi(e);
     const bool pw = want_pw && ensure_tc_wimage(p, st);
+    // channel-block group: all blocks of a tile together when the weights are precomputed (their
+    // entries are then read from HBM about once), tile-major otherwise (values of neighbouring
+    // tiles shared in L2); HEGRID_TC_GROUP overrides
+    int cgroup = pw ? ncb : 1;
+    if (const char* e = getenv("HEGRID_TC_GROUP")) cgroup = std::max(1, std::min(ncb, atoi(e)));
     auto kern = pw ? (sparse ? k_accum_tc<SEG_SPARSE, true> : k_accum_tc<SEG_DENSE, true>)
                    : (sparse ? k_accum_tc<SEG_SPARSE, false> : k_accum_tc<SEG_DENSE, false>);
     HG_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched, p->d_tc_tile_off,
-                                         p->d_tc_wsum, p->d_tc_wimg, p->d_tc_wslot, C, d_out,
-                                         d_weight, dbg);
+                                         p->d_tc_wsum, p->d_tc_wimg, p->d_tc_wslot, C, tiles, cgroup,
+                                         d_out, d_weight, dbg);
     count_launch();
     if (dbg & 32) {
         unsigned long long h[16];
