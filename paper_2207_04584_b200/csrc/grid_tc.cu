@@ -50,7 +50,10 @@ namespace hg {
 
 constexpr int TC_THREADS = 512;
 constexpr int TC_M = 128;                 // channels per CTA (UMMA M)
-constexpr int TC_BX = 4, TC_BY = 3;       // blocks per CTA tile (16 x 12 cells)
+#ifndef HG_TC_BY
+#define HG_TC_BY 3
+#endif
+constexpr int TC_BX = 4, TC_BY = HG_TC_BY; // blocks per CTA tile (16 x 4 TC_BY cells)
 constexpr int TC_NB = TC_BX * TC_BY;      // 12 blocks
 constexpr int TC_N = 16;                  // cells per block: 4 x 4
 constexpr int TC_TW = TC_BX * 4, TC_TH = TC_BY * 4;
@@ -77,7 +80,6 @@ constexpr int TC_KC = 32;                 // samples per chunk (4 MMA K-steps of
 constexpr int NA = HG_TC_NA;              // A stages (TMEM)
 constexpr int NBS = HG_TC_NBS;            // B stages (SMEM)
 constexpr int NV = HG_TC_NV;              // V staging stages (SMEM)
-static_assert(NA == NBS, "A and B stages are released by one commit");
 constexpr int MAXQ = 8;                   // max blocks (B slots) per chunk entry
 // The tensor core's fp32 accumulation truncates, so its error grows with the number of MMAs
 // accumulated into one D element.  D is therefore double-buffered in TMEM by segments of
@@ -123,7 +125,7 @@ struct TcSmem {
     uint4 Es[NV];                         // the chunk's schedule entry (written by the V loader)
     uint32_t Bmask[NBF];                  // block mask of the chunk in each weight stage / ring entry
     uint32_t Boff[NBF];                   // PW: ring offset of the entry
-    // A stage s and B stage s hold the same chunk (NA == NBS)
+    // chunk c: A stage c % NA, B stage c % NBS (OTF) or ring entry c % NBF (PW)
     uint64_t a_full[NA], b_full[NBF], done[NBF], v_full[NV], v_empty[NV];
     uint64_t seg_done[2], seg_free[2];    // D buffer d: segment's MMAs complete / promoted
     uint64_t bar_done;
@@ -497,6 +499,11 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_raw);
     if (tc::smem_u32(smem_raw) & 1023u) __trap();   // swizzle atoms need 1024-B alignment
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // A producers: warps 4-7, plus 8-11 when the weights are precomputed (those warps are the
+    // B producers otherwise); each lane quarter's chunk columns are split between its warps
+    constexpr int A_WARPS = PW ? 8 : 4, A_GROUPS = A_WARPS / 4, A_THREADS = 32 * A_WARPS;
+    constexpr int KPW = TC_KC / A_GROUPS;
+    constexpr int NI = PW ? (TC_BY < 3 ? TC_BY : 3) : 2;   // MMA issuer warps
 #ifdef HG_TC_PROF
     // debug switches (HEGRID_TC_DEBUG) and cycle counters: only in profiling builds
     const int dbg = dbg_in;
@@ -529,20 +536,20 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 
     if (warp == 0) tc::tmem_alloc(&sm.tmem_base, TMEM_COLS);
     if (tid == 32) {
-        for (int s = 0; s < NA; ++s) tc::mbar_init(&sm.a_full[s], 128);
+        for (int s = 0; s < NA; ++s) tc::mbar_init(&sm.a_full[s], A_THREADS);
         for (int s = 0; s < NBF; ++s) {
-            tc::mbar_init(&sm.done[s], 1);
+            tc::mbar_init(&sm.done[s], NI);           // one commit per issuer
             tc::mbar_init(&sm.b_full[s], PW ? 1 : W_THREADS);   // PW: the weight loader's tx
         }
         for (int s = 0; s < NV; ++s) {
             tc::mbar_init(&sm.v_full[s], 1);
-            tc::mbar_init(&sm.v_empty[s], PW ? 128 : 128 + W_THREADS);
+            tc::mbar_init(&sm.v_empty[s], PW ? A_THREADS : A_THREADS + W_THREADS);
         }
         for (int d = 0; d < 2; ++d) {
-            tc::mbar_init(&sm.seg_done[d], 1);
-            tc::mbar_init(&sm.seg_free[d], 128);
+            tc::mbar_init(&sm.seg_done[d], NI);
+            tc::mbar_init(&sm.seg_free[d], A_THREADS);
         }
-        tc::mbar_init(&sm.bar_done, 1);
+        tc::mbar_init(&sm.bar_done, NI);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     {   // the master sums start at 0
@@ -568,12 +575,14 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 
     // D buffer d -> master: this warp's lane quarter (channels), blocks in `mask`; with
     // rezero, the blocks are cleared for the buffer's next segment
+    // With 8 A warps (PW), the two warps of a lane quarter take alternate blocks.
     auto promote_buffer = [&](int d, uint32_t mask, bool rezero) {
-        const int q4 = warp & 3, row = q4 * 32 + lane;
+        const int q4 = warp & 3, row = q4 * 32 + lane, grp = (warp - 4) >> 2;
         float* mrow = &sm.M[row][0];
-        while (mask) {
+        for (int i = 0; mask; ++i) {
             const int b = __ffs(mask) - 1;
             mask &= mask - 1;
+            if (i % A_GROUPS != grp) continue;
             uint32_t r[16];
             const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)d * D_COLS + (uint32_t)(b * TC_N);
             tc::tmem_ld16(ta, r);
@@ -603,11 +612,19 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     const int nseg = (nchunks + SEG - 1) / SEG;
     auto promoted_in_loop = [&](int s) { return (s + 1) * SEG + NA <= nchunks - 1; };
 
-    if (warp == 0) {
+    // MMA issuers: issuer i (warps 0, 3 and, with precomputed weights, 13 -- on different SM
+    // sub-partitions) issues the MMAs of the tile's block rows r with r % NI == i, so the
+    // per-MMA issue cost is spread over NI instruction streams.  Each D column block is always
+    // fed by the same issuer in chunk order: the accumulation order stays fixed.
+    const int issuer = warp == 0 ? 0 : warp == 3 ? 1 : (NI > 2 && warp == 13) ? 2 : -1;
+    if (issuer >= 0) {
         // ============================ MMA issuer =============================
         // chunk c uses A stage c % NA; the loop is unrolled by NA so the stage (and with it
         // every A operand address) is a compile-time constant in each body
-        static_assert(NA == 2, "issuer unrolled for two A stages");
+        uint32_t rows = 0;
+        for (int b = 0; b < TC_NB; ++b)
+            if ((b / TC_BX) % NI == issuer) rows |= 1u << b;
+        static_assert(NA == 2 || NA == 4, "issuer unrolled for two or four A stages");
         auto issue = [&](const int c, auto SA_) {
             constexpr int sa = decltype(SA_)::value;
             const int seg = c / SEG, d = seg & 1;
@@ -646,16 +663,15 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 const uint32_t dh0 = tc::sdesc_sw128_lo(b_addr);
                 const uint32_t a0 = tmem + A_COL0 + sa * 64;
                 const uint32_t dbase = tmem + (uint32_t)d * D_COLS;
-                uint32_t mm = mask;
-                int q = 0;
+                uint32_t mm = mask & rows;
                 while (mm) {
                     const int b = __ffs(mm) - 1;
                     const int r = __ffs(~(mm >> b)) - 1;
                     mm &= ~(((1u << r) - 1u) << b);
+                    const int q = __popc(mask & ((1u << b) - 1u));     // B slot of block b
                     const uint32_t bh = dh0 + (uint32_t)((q * SLOT_BYTES) >> 4);
                     tc::mma12_3xtf32<(32 >> 4)>(dbase + (uint32_t)(b * TC_N), a0, bh, bh + (uint32_t)lo16,
                                                 tc::idesc_tf32(TC_M, TC_N * r));
-                    q += r;
                 }
             }
             tc::mma_commit_warp(&sm.done[c % NBF]);    // a commit costs ~100 cycles: one per chunk
@@ -664,11 +680,19 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             TPROF_END(2);
         };
         int c = 0;
-        for (; c + 1 < nchunks; c += 2) {
+        for (; c + NA - 1 < nchunks; c += NA) {
             issue(c, std::integral_constant<int, 0>{});
             issue(c + 1, std::integral_constant<int, 1>{});
+            if constexpr (NA == 4) {
+                issue(c + 2, std::integral_constant<int, 2>{});
+                issue(c + 3, std::integral_constant<int, 3>{});
+            }
         }
         if (c < nchunks) issue(c, std::integral_constant<int, 0>{});
+        if constexpr (NA == 4) {
+            if (c + 1 < nchunks) issue(c + 1, std::integral_constant<int, 1>{});
+            if (c + 2 < nchunks) issue(c + 2, std::integral_constant<int, 2>{});
+        }
         tc::mma_commit_warp(&sm.bar_done);
         __syncwarp();
     } else if (warp == 1) {
@@ -721,55 +745,86 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         // entry c's nq x 4 KB of precomputed weights -> the ring at the next contiguous offset
         // (wrapping to 0); the bytes are reused once every chunk placed there has completed
         // (done[] phases, confirmed in order).  At most NBF entries are in flight.
+        // Entry masks and slots are read in groups of G, two groups ahead, into registers
+        // (static indices), so no global-load latency sits on the loop; the entries of the next
+        // group are prefetched into L2 one group ahead.
         if (lane == 0) {
             const uint32_t* ws = wslot + tile_off[tile];
+            constexpr int G = 8;
+            uint32_t zc[G], sc[G], zn[G], sn[G], zf[G], sf[G];
+            auto ldg = [&](int g0, uint32_t (&z)[G], uint32_t (&sl)[G]) {
+#pragma unroll
+                for (int u = 0; u < G; ++u) {
+                    const int c = g0 + u;
+                    z[u] = c < nchunks ? __ldg(&cs[c].z) : 0u;
+                    sl[u] = c < nchunks ? __ldg(&ws[c]) : 0u;
+                }
+            };
+            auto pf = [&](const uint32_t (&z)[G], const uint32_t (&sl)[G]) {
+#pragma unroll
+                for (int u = 0; u < G; ++u)
+                    if (z[u]) tc::prefetch_l2(wimg + (size_t)sl[u] * (2u * SLOT_BYTES), __popc(z[u]) * 2u * SLOT_BYTES);
+            };
+            ldg(0, zc, sc);
+            ldg(G, zn, sn);
+            ldg(2 * G, zf, sf);
+            pf(zc, sc);
+            pf(zn, sn);
             long long head = 0, starts[NBF];
             int conf = 0;                         // chunks confirmed complete
-            constexpr int WPF = 8;                // L2 prefetch distance (entries)
-            for (int c = 0; c < WPF && c < nchunks; ++c)
-                tc::prefetch_l2(wimg + (size_t)__ldg(&ws[c]) * (2u * SLOT_BYTES), __popc(__ldg(&cs[c].z)) * 2u * SLOT_BYTES);
-            for (int c = 0; c < nchunks; ++c) {
-                const uint4 e = __ldg(&cs[c]);
-                const uint32_t nq = __popc(e.z), bytes = nq * 2u * SLOT_BYTES;
-                if (c + WPF < nchunks)
-                    tc::prefetch_l2(wimg + (size_t)__ldg(&ws[c + WPF]) * (2u * SLOT_BYTES),
-                                    __popc(__ldg(&cs[c + WPF].z)) * 2u * SLOT_BYTES);
-                long long off = head % RING;
-                if (off + bytes > RING) {
-                    head += RING - off;
-                    off = 0;
+            for (int g0 = 0; g0 < nchunks; g0 += G) {
+#pragma unroll
+                for (int u = 0; u < G; ++u) {
+                    const int c = g0 + u;
+                    if (c >= nchunks) break;
+                    const uint32_t bytes = __popc(zc[u]) * 2u * SLOT_BYTES;
+                    long long off = head % RING;
+                    if (off + bytes > RING) {
+                        head += RING - off;
+                        off = 0;
+                    }
+                    TPROF_BEGIN;
+                    // reuse: the slot barrier of chunk c - NBF, and every chunk that started less
+                    // than one ring length before this entry's end
+                    while (conf < c && (c - conf >= NBF || starts[conf % NBF] < head + (long long)bytes - RING)) {
+                        tc::mbar_wait(&sm.done[conf % NBF], (conf / NBF) & 1);
+                        ++conf;
+                    }
+                    TPROF_END(0);
+                    starts[c % NBF] = head;
+                    const int k = c % NBF;
+                    sm.Bmask[k] = zc[u];
+                    sm.Boff[k] = (uint32_t)off;
+                    tc::mbar_arrive_expect_tx(&sm.b_full[k], bytes);
+                    tc::bulk_g2s(&sm.B[off], wimg + (size_t)sc[u] * (2u * SLOT_BYTES), bytes, &sm.b_full[k]);
+                    head += bytes;
                 }
-                TPROF_BEGIN;
-                // reuse: the slot barrier of chunk c - NBF, and every chunk that started less than
-                // one ring length before this entry's end
-                while (conf < c && (c - conf >= NBF || starts[conf % NBF] < head + (long long)bytes - RING)) {
-                    tc::mbar_wait(&sm.done[conf % NBF], (conf / NBF) & 1);
-                    ++conf;
+#pragma unroll
+                for (int u = 0; u < G; ++u) {
+                    zc[u] = zn[u];
+                    sc[u] = sn[u];
+                    zn[u] = zf[u];
+                    sn[u] = sf[u];
                 }
-                TPROF_END(0);
-                starts[c % NBF] = head;
-                const int k = c % NBF;
-                sm.Bmask[k] = e.z;
-                sm.Boff[k] = (uint32_t)off;
-                tc::fence_after_sync();
-                tc::mbar_arrive_expect_tx(&sm.b_full[k], bytes);
-                tc::bulk_g2s(&sm.B[off], wimg + (size_t)__ldg(&ws[c]) * (2u * SLOT_BYTES), bytes, &sm.b_full[k]);
-                head += bytes;
+                ldg(g0 + 3 * G, zf, sf);
+                pf(zn, sn);
             }
         }
         __syncwarp();
     }
     // A producers keep the block masks of the (at most two) segments not yet promoted
     uint32_t segmask0 = 0u, segmask1 = 0u;   // (scalars: no local-memory array)
-    if (warp >= 4 && warp < 8) {
+    if (warp >= 4 && warp < 4 + A_WARPS) {
         // ============================ A producers ============================
+        // warp (4 + 4 g + q): lane quarter q (TMEM lanes = channels), samples [k0, k0 + KPW)
         const int q4 = warp & 3;
         const int chl = q4 * 32 + lane;            // channel within the block = TMEM lane
+        const int k0 = ((warp - 4) >> 2) * KPW;
         // channels >= C arrive as zeros (the tensor map's out-of-range fill)
         const bool ch_ok = !(dbg & 4);
         // Software-pipelined: the values of chunk c+1 are loaded and split while chunk c's
         // tcgen05.st is in flight; chunk c is published (a_full) once its stores completed.
-        uint32_t hi[TC_KC], lo[TC_KC];
+        uint32_t hi[KPW], lo[KPW];
         auto load_split = [&](int c) {
             const int sv = c % NV;
             {
@@ -777,20 +832,29 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 tc::mbar_wait(&sm.v_full[sv], (c / NV) & 1);
                 TPROF_END(0);
             }
-            const float* vs = reinterpret_cast<const float*>(&sm.Vs[sv][0]) + chl;
+            const float* vs = reinterpret_cast<const float*>(&sm.Vs[sv][0]) + k0 * TC_M + chl;
             const uint4 ee = sm.Es[sv];
             const uint32_t nk = ee.y & 63;
             if ((c / SEG) & 1) segmask1 |= ee.z; else segmask0 |= ee.z;
             if (nk == TC_KC && ch_ok) {            // full chunk: no masking
 #pragma unroll
-                for (int k = 0; k < TC_KC; ++k) tc::split_tf32(vs[k * TC_M], hi[k], lo[k]);
+                for (int k = 0; k < KPW; ++k) tc::split_tf32(vs[k * TC_M], hi[k], lo[k]);
             } else {                                // rows >= nk belong to other chunks
 #pragma unroll
-                for (int k = 0; k < TC_KC; ++k) {
-                    const float v = ((uint32_t)k < nk && ch_ok) ? vs[k * TC_M] : 0.0f;
+                for (int k = 0; k < KPW; ++k) {
+                    const float v = ((uint32_t)(k0 + k) < nk && ch_ok) ? vs[k * TC_M] : 0.0f;
                     tc::split_tf32(v, hi[k], lo[k]);
                 }
             }
+            // The values now live in registers: release the value stage (the V loader refills
+            // it while this chunk still waits for its A stage).  An mbarrier arrive does not
+            // wait for outstanding shared loads, so a store of the xor of every split result
+            // (which cannot issue before all loads returned) goes first.
+            uint32_t dep = ee.x ^ ee.y ^ ee.z;
+#pragma unroll
+            for (int k = 0; k < KPW; ++k) dep ^= lo[k] ^ hi[k];
+            asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[warp])), "r"(dep) : "memory");
+            tc::mbar_arrive(&sm.v_empty[sv]);
         };
         auto store = [&](int c) {
             const int sa = c % NA;
@@ -800,11 +864,14 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 TPROF_END(1);
             }
             tc::fence_after_sync();
-            const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + A_COL0 + sa * 64;
-            tc::tmem_st32(ta, hi);
-            tc::tmem_st32(ta + 32, lo);
-            // the tcgen05.st consumed every value loaded from the stage: release it
-            tc::mbar_arrive(&sm.v_empty[c % NV]);
+            const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + A_COL0 + sa * 64 + k0;
+            if constexpr (KPW == 32) {
+                tc::tmem_st32(ta, hi);
+                tc::tmem_st32(ta + 32, lo);
+            } else {
+                tc::tmem_st16(ta, hi);
+                tc::tmem_st16(ta + 32, lo);
+            }
         };
         if (nchunks > 0) {
             load_split(0);
@@ -898,7 +965,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     // master tile to out: V = S / W (Eq. 1's division), NaN where W = 0
     tc::mbar_wait(&sm.bar_done, 0);
     tc::fence_after_sync();
-    if (warp >= 4 && warp < 8) {
+    if (warp >= 4 && warp < 4 + A_WARPS) {
         for (int s = (nseg >= 2 ? nseg - 2 : 0); s < nseg; ++s)
             if (!promoted_in_loop(s)) promote_buffer(s & 1, (s & 1) ? segmask1 : segmask0, false);
     }

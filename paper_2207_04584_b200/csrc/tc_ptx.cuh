@@ -46,6 +46,16 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 #define HG_MBAR_SUSPEND_NS 1000000
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef HG_MBAR_SPIN
+    // spin on the non-blocking test (no suspension: lowest wake-up latency)
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t"
+        "}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+#else
     asm volatile(
         "{\n\t"
         ".reg .pred p;\n\t"
@@ -53,6 +63,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t"
         "}\n" :: "r"(smem_u32(bar)), "r"(parity), "n"(HG_MBAR_SUSPEND_NS) : "memory");
+#endif
 }
 // Kept for the roles that usually run ahead (same wait; the hint already suspends).
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
