@@ -131,6 +131,7 @@ struct TcSmem {
     uint64_t bar_done;
     uint32_t tmem_base;
     uint32_t sink[TC_THREADS / 32];       // dependency sink (see the B producers' release)
+    float Wt[TC_TW * TC_TH];              // the tile's W per cell (epilogue)
     alignas(16) float M[TC_M][T_LD];      // fp32 master sums [channel][cell] (padded rows)
 };
 
@@ -705,8 +706,10 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         static_assert(PF < 32, "prefetch distance must stay within the next entry batch");
         auto ld_entry = [&](int c) { return c < nchunks ? __ldg(&cs[c]) : make_uint4(0, 0, 0, 0); };
         uint4 cur = ld_entry(lane), nxt = ld_entry(32 + lane);
+#ifndef HG_TC_NO_VPF
         if (lane == 0)
             for (int c = 0; c < PF && c < nchunks; ++c) tc::tma_prefetch_2d(&tmap_v, cb, (int)__ldg(&cs[c].x));
+#endif
         for (int c = 0; c < nchunks; ++c) {
             if ((c & 31) == 0 && c > 0) {
                 cur = nxt;
@@ -722,7 +725,9 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             if (lane == 0) {
                 const uint32_t nk = e.y & 63;
                 const int sv = c % NV;
+#ifndef HG_TC_NO_VPF
                 if (cp < nchunks) tc::tma_prefetch_2d(&tmap_v, cb, (int)xp);
+#endif
                 {
                     TPROF_BEGIN;
                     if (c >= NV) tc::mbar_wait(&sm.v_empty[sv], ((c / NV) - 1) & 1);
@@ -746,8 +751,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         // (wrapping to 0); the bytes are reused once every chunk placed there has completed
         // (done[] phases, confirmed in order).  At most NBF entries are in flight.
         // Entry masks and slots are read in groups of G, two groups ahead, into registers
-        // (static indices), so no global-load latency sits on the loop; the entries of the next
-        // group are prefetched into L2 one group ahead.
+        // (static indices), so no global-load latency sits on the loop.  (An L2 prefetch of
+        // the next group's weights, HG_TC_WPF, measured slower: the CTAs of a tile share them.)
         if (lane == 0) {
             const uint32_t* ws = wslot + tile_off[tile];
             constexpr int G = 8;
@@ -761,9 +766,11 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 }
             };
             auto pf = [&](const uint32_t (&z)[G], const uint32_t (&sl)[G]) {
+#ifdef HG_TC_WPF
 #pragma unroll
                 for (int u = 0; u < G; ++u)
                     if (z[u]) tc::prefetch_l2(wimg + (size_t)sl[u] * (2u * SLOT_BYTES), __popc(z[u]) * 2u * SLOT_BYTES);
+#endif
             };
             ldg(0, zc, sc);
             ldg(G, zn, sn);
@@ -969,17 +976,21 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         for (int s = (nseg >= 2 ? nseg - 2 : 0); s < nseg; ++s)
             if (!promoted_in_loop(s)) promote_buffer(s & 1, (s & 1) ? segmask1 : segmask0, false);
     }
+    if (tid < TC_TW * TC_TH) {
+        const int i = i0 + tid % TC_TW, j = j0 + tid / TC_TW;
+        sm.Wt[tid] = (i < g.nx && j < g.ny) ? __ldg(&wsum[(int64_t)j * g.nx + i]) : 0.0f;
+    }
     __syncthreads();
     {
         const float qnan = __int_as_float(0x7fc00000);
         const int x = lane & 15;
-#pragma unroll 2
+#pragma unroll 4
         for (int it = warp; it < TC_M * (TC_TH / 2); it += TC_THREADS / 32) {
             const int row = it / (TC_TH / 2), y = (it % (TC_TH / 2)) * 2 + (lane >> 4);
             const int ch = cb + row, i = i0 + x, j = j0 + y;
             if (ch < C && i < g.nx && j < g.ny) {
                 const float S = sm.M[row][y * TC_TW + x];
-                const float W = __ldg(&wsum[(int64_t)j * g.nx + i]);
+                const float W = sm.Wt[y * TC_TW + x];
                 out[(int64_t)ch * cells + (int64_t)j * g.nx + i] = W > 0.0f ? __fdiv_rn(S, W) : qnan;
             }
         }
