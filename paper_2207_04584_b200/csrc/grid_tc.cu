@@ -37,6 +37,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <chrono>
 #include <type_traits>
 #include <vector>
 
@@ -373,9 +374,20 @@ k_tc_wimage(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict_
 
 // Build the weight image once per plan (first launch that asks for it).  Returns false (and
 // leaves the plan in on-the-fly mode) if the image does not fit the memory budget.
+// HEGRID_TC_TIMING=1 prints the host-side phases of the one-time per-plan preparation
+static void prep_mark(const char* what) {
+    static const bool on = getenv("HEGRID_TC_TIMING") != nullptr;
+    static auto t0 = std::chrono::steady_clock::now();
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[tc prep] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+}
+
 static bool ensure_tc_wimage(const hegrid_plan_s* p, cudaStream_t st) {
     if (p->tc_pw >= 0) return p->tc_pw == 1;
     p->tc_pw = 0;
+    prep_mark("wimage start");
     const Geom& g = p->g;
     const int tiles = ((g.nx + TC_TW - 1) / TC_TW) * ((g.ny + TC_TH - 1) / TC_TH);
     const int64_t ne = p->tc_nchunks;
@@ -384,6 +396,7 @@ static bool ensure_tc_wimage(const hegrid_plan_s* p, cudaStream_t st) {
     if (cudaMemcpyAsync(h.data(), p->d_tc_sched, ne * sizeof(uint4), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
         return false;
+    prep_mark("schedule to host");
     std::vector<uint32_t> slot(ne);
     uint64_t tot = 0;
     for (int64_t i = 0; i < ne; ++i) {
@@ -395,7 +408,9 @@ static bool ensure_tc_wimage(const hegrid_plan_s* p, cudaStream_t st) {
     if (tot >= (1ull << 32) || cudaMemGetInfo(&fr, &total) != cudaSuccess || bytes > fr / 4) return false;
     uint8_t* d_img = nullptr;
     uint32_t* d_slot = nullptr;
+    prep_mark("slot scan + meminfo");
     if (cudaMalloc(&d_img, bytes) != cudaSuccess) return false;
+    prep_mark("image cudaMalloc");
     if (cudaMalloc(&d_slot, ne * sizeof(uint32_t)) != cudaSuccess) {
         cudaFree(d_img);
         return false;
@@ -407,6 +422,7 @@ static bool ensure_tc_wimage(const hegrid_plan_s* p, cudaStream_t st) {
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    prep_mark("image kernel");
     if (e != cudaSuccess) {
         cudaFree(d_img);
         cudaFree(d_slot);
@@ -421,6 +437,7 @@ static bool ensure_tc_wimage(const hegrid_plan_s* p, cudaStream_t st) {
 
 static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     if (p->tc_nchunks >= 0) return HEGRID_OK;
+    prep_mark("schedule start");
     const Geom& g = p->g;
     const int tiles = ((g.nx + TC_TW - 1) / TC_TW) * ((g.ny + TC_TH - 1) / TC_TH);
     const int64_t cells = (int64_t)g.nx * g.ny;
@@ -469,6 +486,7 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
         if (d_s) cudaFree(d_s);
         return cuda_status(e);
     }
+    prep_mark("schedule + wsum built");
     p->d_tc_sched = d_s;
     p->d_tc_tile_off = d_n;
     p->d_tc_wsum = d_w;
@@ -494,8 +512,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
            PlanDev pd, const uint4* __restrict__ sched,
            const uint32_t* __restrict__ tile_off, const float* __restrict__ wsum,
            const uint8_t* __restrict__ wimg, const uint32_t* __restrict__ wslot,
-           int C, int tiles, int cgroup, float* __restrict__ out, float* __restrict__ wout,
-           int dbg_in) {
+           int C, int tiles, int cgroup, int super_, int snake, float* __restrict__ out,
+           float* __restrict__ wout, int dbg_in) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_raw);
     if (tc::smem_u32(smem_raw) & 1023u) __trap();   // swizzle atoms need 1024-B alignment
@@ -526,13 +544,25 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         const int ncb = (C + TC_M - 1) / TC_M;
         const int lin = blockIdx.x, grp = lin / (tiles * cgroup), within = lin % (tiles * cgroup);
         const int gsz = min(cgroup, ncb - grp * cgroup);
-        tile = within / gsz;
+        const int L = within / gsz;
         cblk = grp * cgroup + within % gsz;
+        // tile L of the walk: S x S super-tiles (row-major), row-major inside each, so the
+        // tiles resident together are 2-D neighbours and share their candidate samples in L2
+        const int S = super_, tiles_y = tiles / tiles_x;
+        const int band = L / (S * tiles_x), h = min(S, tiles_y - band * S);
+        const int bl = L - band * S * tiles_x, sx = bl / (h * S);
+        const int w = min(S, tiles_x - sx * S), local = bl - sx * h * S;
+        tile = (band * S + local / w) * tiles_x + sx * S + local % w;
     }
     const int i0 = (tile % tiles_x) * TC_TW, j0 = (tile / tiles_x) * TC_TH;
     const int cb = cblk * TC_M;
     const uint4* cs = sched + tile_off[tile];
     const int nchunks = (int)(tile_off[tile + 1] - tile_off[tile]);
+    // Tiles of odd tile rows walk their entries backwards (bottom bin rows first): a tile and
+    // the one below it then read the bin rows they share at the same stage of their lifetimes,
+    // while both are resident, so the second read hits L2.  The order is fixed per tile.
+    const bool rev = (snake != 0) && (((tile / tiles_x) & 1) != 0);
+    auto ent = [&](int c) { return rev ? nchunks - 1 - c : c; };
     const int64_t cells = (int64_t)g.nx * g.ny;
 
     if (warp == 0) tc::tmem_alloc(&sm.tmem_base, TMEM_COLS);
@@ -704,11 +734,11 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         // batch ahead, and hands each chunk's entry to the consumers through Es[stage]
         constexpr int PF = NV + 3;
         static_assert(PF < 32, "prefetch distance must stay within the next entry batch");
-        auto ld_entry = [&](int c) { return c < nchunks ? __ldg(&cs[c]) : make_uint4(0, 0, 0, 0); };
+        auto ld_entry = [&](int c) { return c < nchunks ? __ldg(&cs[ent(c)]) : make_uint4(0, 0, 0, 0); };
         uint4 cur = ld_entry(lane), nxt = ld_entry(32 + lane);
 #ifndef HG_TC_NO_VPF
         if (lane == 0)
-            for (int c = 0; c < PF && c < nchunks; ++c) tc::tma_prefetch_2d(&tmap_v, cb, (int)__ldg(&cs[c].x));
+            for (int c = 0; c < PF && c < nchunks; ++c) tc::tma_prefetch_2d(&tmap_v, cb, (int)__ldg(&cs[ent(c)].x));
 #endif
         for (int c = 0; c < nchunks; ++c) {
             if ((c & 31) == 0 && c > 0) {
@@ -761,8 +791,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 #pragma unroll
                 for (int u = 0; u < G; ++u) {
                     const int c = g0 + u;
-                    z[u] = c < nchunks ? __ldg(&cs[c].z) : 0u;
-                    sl[u] = c < nchunks ? __ldg(&ws[c]) : 0u;
+                    z[u] = c < nchunks ? __ldg(&cs[ent(c)].z) : 0u;
+                    sl[u] = c < nchunks ? __ldg(&ws[ent(c)]) : 0u;
                 }
             };
             auto pf = [&](const uint32_t (&z)[G], const uint32_t (&sl)[G]) {
@@ -1080,12 +1110,15 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     // tiles shared in L2); HEGRID_TC_GROUP overrides
     int cgroup = pw ? ncb : 1;
     if (const char* e = getenv("HEGRID_TC_GROUP")) cgroup = std::max(1, std::min(ncb, atoi(e)));
+    int super_ = 1, snake = 0;
+    if (const char* e = getenv("HEGRID_TC_SUPER")) super_ = std::max(1, atoi(e));
+    if (const char* e = getenv("HEGRID_TC_SNAKE")) snake = atoi(e);
     auto kern = pw ? (sparse ? k_accum_tc<SEG_SPARSE, true> : k_accum_tc<SEG_DENSE, true>)
                    : (sparse ? k_accum_tc<SEG_SPARSE, false> : k_accum_tc<SEG_DENSE, false>);
     HG_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched, p->d_tc_tile_off,
                                          p->d_tc_wsum, p->d_tc_wimg, p->d_tc_wslot, C, tiles, cgroup,
-                                         d_out, d_weight, dbg);
+                                         super_, snake, d_out, d_weight, dbg);
     count_launch();
     if (dbg & 32) {
         unsigned long long h[16];

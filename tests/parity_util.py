@@ -69,4 +69,10 @@ def engine_env(engine, monkeypatch):
     if engine in ("tc_pw", "tc_otf"):
         monkeypatch.setenv("HEGRID_TC_PW", "1" if engine == "tc_pw" else "0")
         return "tc"
+    if engine == "tc_pw_walk":     # ragged channel-block groups, 3x3 super-tile walk
+        monkeypatch.setenv("HEGRID_TC_PW", "1")
+        monkeypatch.setenv("HEGRID_TC_GROUP", "2")
+        monkeypatch.setenv("HEGRID_TC_SUPER", "3")
+        monkeypatch.setenv("HEGRID_TC_SNAKE", "1")
+        return "tc"
     return engine

@@ -18,7 +18,7 @@ from parity_util import compare, engine_env, make_inputs, oracle_grid, plan_layo
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = ["simt", "tc", "tc_pw"]
+ENGINES = ["simt", "tc", "tc_pw", "tc_pw_walk"]
 
 
 # ------------------------------------------------------------------ plan layer
