@@ -49,6 +49,13 @@
 
 namespace hg {
 
+// waits of the single-warp roles on the critical hand-off chain (issuers, weight loader)
+#ifdef HG_CRIT_SPIN
+#define HG_WAIT_CRIT(b, p) tc::mbar_wait_spin((b), (p))
+#else
+#define HG_WAIT_CRIT(b, p) tc::mbar_wait((b), (p))
+#endif
+
 constexpr int TC_THREADS = 512;
 constexpr int TC_M = 128;                 // channels per CTA (UMMA M)
 #ifndef HG_TC_BY
@@ -567,18 +574,18 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 
     if (warp == 0) tc::tmem_alloc(&sm.tmem_base, TMEM_COLS);
     if (tid == 32) {
-        for (int s = 0; s < NA; ++s) tc::mbar_init(&sm.a_full[s], A_THREADS);
+        for (int s = 0; s < NA; ++s) tc::mbar_init(&sm.a_full[s], A_WARPS);   // one arrive per warp
         for (int s = 0; s < NBF; ++s) {
             tc::mbar_init(&sm.done[s], NI);           // one commit per issuer
-            tc::mbar_init(&sm.b_full[s], PW ? 1 : W_THREADS);   // PW: the weight loader's tx
+            tc::mbar_init(&sm.b_full[s], PW ? 1 : W_THREADS / 32);   // PW: the weight loader's tx
         }
         for (int s = 0; s < NV; ++s) {
             tc::mbar_init(&sm.v_full[s], 1);
-            tc::mbar_init(&sm.v_empty[s], PW ? A_THREADS : A_THREADS + W_THREADS);
+            tc::mbar_init(&sm.v_empty[s], PW ? A_WARPS : A_WARPS + W_THREADS / 32);
         }
         for (int d = 0; d < 2; ++d) {
             tc::mbar_init(&sm.seg_done[d], NI);
-            tc::mbar_init(&sm.seg_free[d], A_THREADS);
+            tc::mbar_init(&sm.seg_free[d], A_WARPS);
         }
         tc::mbar_init(&sm.bar_done, NI);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -610,6 +617,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     auto promote_buffer = [&](int d, uint32_t mask, bool rezero) {
         const int q4 = warp & 3, row = q4 * 32 + lane, grp = (warp - 4) >> 2;
         float* mrow = &sm.M[row][0];
+        if (dbg & 1024) mask = 0;
         for (int i = 0; mask; ++i) {
             const int b = __ffs(mask) - 1;
             mask &= mask - 1;
@@ -664,7 +672,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 // (segment seg - 2) and zeroed
                 if (seg >= 2) {
                     TPROF_BEGIN;
-                    tc::mbar_wait(&sm.seg_free[d], ((seg >> 1) - 1) & 1);
+                    HG_WAIT_CRIT(&sm.seg_free[d], ((seg >> 1) - 1) & 1);
                     TPROF_END(3);
                     tc::fence_after_sync();
                 }
@@ -672,12 +680,12 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const int sb = PW ? c % NBF : c % NBS;
             {
                 TPROF_BEGIN;
-                tc::mbar_wait(&sm.a_full[sa], (c / NA) & 1);
+                HG_WAIT_CRIT(&sm.a_full[sa], (c / NA) & 1);
                 TPROF_END(0);
             }
             {
                 TPROF_BEGIN;
-                tc::mbar_wait(&sm.b_full[sb], PW ? (c / NBF) & 1 : (c / NBS) & 1);
+                HG_WAIT_CRIT(&sm.b_full[sb], PW ? (c / NBF) & 1 : (c / NBS) & 1);
                 TPROF_END(1);
             }
             tc::fence_after_sync();
@@ -814,7 +822,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 for (int u = 0; u < G; ++u) {
                     const int c = g0 + u;
                     if (c >= nchunks) break;
-                    const uint32_t bytes = __popc(zc[u]) * 2u * SLOT_BYTES;
+                    const uint32_t bytes = (dbg & 2048) ? 0u : __popc(zc[u]) * 2u * SLOT_BYTES;
                     long long off = head % RING;
                     if (off + bytes > RING) {
                         head += RING - off;
@@ -824,7 +832,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     // reuse: the slot barrier of chunk c - NBF, and every chunk that started less
                     // than one ring length before this entry's end
                     while (conf < c && (c - conf >= NBF || starts[conf % NBF] < head + (long long)bytes - RING)) {
-                        tc::mbar_wait(&sm.done[conf % NBF], (conf / NBF) & 1);
+                        HG_WAIT_CRIT(&sm.done[conf % NBF], (conf / NBF) & 1);
                         ++conf;
                     }
                     TPROF_END(0);
@@ -832,8 +840,12 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     const int k = c % NBF;
                     sm.Bmask[k] = zc[u];
                     sm.Boff[k] = (uint32_t)off;
-                    tc::mbar_arrive_expect_tx(&sm.b_full[k], bytes);
-                    tc::bulk_g2s(&sm.B[off], wimg + (size_t)sc[u] * (2u * SLOT_BYTES), bytes, &sm.b_full[k]);
+                    if (dbg & 512) {
+                        tc::mbar_arrive(&sm.b_full[k]);
+                    } else {
+                        tc::mbar_arrive_expect_tx(&sm.b_full[k], bytes);
+                        tc::bulk_g2s(&sm.B[off], wimg + (size_t)sc[u] * (2u * SLOT_BYTES), bytes, &sm.b_full[k]);
+                    }
                     head += bytes;
                 }
 #pragma unroll
@@ -873,7 +885,10 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const uint4 ee = sm.Es[sv];
             const uint32_t nk = ee.y & 63;
             if ((c / SEG) & 1) segmask1 |= ee.z; else segmask0 |= ee.z;
-            if (nk == TC_KC && ch_ok) {            // full chunk: no masking
+            if (dbg & 256) {                        // debug: no value work
+#pragma unroll
+                for (int k = 0; k < KPW; ++k) { hi[k] = 0u; lo[k] = 0u; }
+            } else if (nk == TC_KC && ch_ok) {     // full chunk: no masking
 #pragma unroll
                 for (int k = 0; k < KPW; ++k) tc::split_tf32(vs[k * TC_M], hi[k], lo[k]);
             } else {                                // rows >= nk belong to other chunks
@@ -891,7 +906,9 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 #pragma unroll
             for (int k = 0; k < KPW; ++k) dep ^= lo[k] ^ hi[k];
             asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[warp])), "r"(dep) : "memory");
-            tc::mbar_arrive(&sm.v_empty[sv]);
+            // one arrive per warp (hundreds of per-thread arrives on one mbarrier serialise)
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sm.v_empty[sv]);
         };
         auto store = [&](int c) {
             const int sa = c % NA;
@@ -902,7 +919,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             }
             tc::fence_after_sync();
             const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + A_COL0 + sa * 64 + k0;
-            if constexpr (KPW == 32) {
+            if (dbg & 256) {
+            } else if constexpr (KPW == 32) {
                 tc::tmem_st32(ta, hi);
                 tc::tmem_st32(ta + 32, lo);
             } else {
@@ -922,7 +940,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             }
             tc::wait_st();
             tc::fence_before_sync();
-            tc::mbar_arrive(&sm.a_full[c % NA]);
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sm.a_full[c % NA]);
             if (c + 1 < nchunks) {
                 const int cn = c + 1;
                 if (cn >= SEG && cn % SEG == NA) {
@@ -936,7 +955,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     if (d) segmask1 = 0; else segmask0 = 0;
                     tc::wait_st();
                     tc::fence_before_sync();
-                    tc::mbar_arrive(&sm.seg_free[d]);
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(&sm.seg_free[d]);
                     TPROF_END(2);
                 }
                 store(cn);
@@ -976,7 +996,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     dep ^= __float_as_uint(g4[u].x) ^ __float_as_uint(g4[u].y) ^
                            __float_as_uint(g4[u].z) ^ __float_as_uint(g4[u].w);
                 asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[warp])), "r"(dep) : "memory");
-                tc::mbar_arrive(&sm.v_empty[sv]);
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&sm.v_empty[sv]);
             }
 
             const int sb = c % NBS;
@@ -991,7 +1012,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             entry_weights(g, pd, i0, j0, wt, cosr, g4, pstart, row, blist, nq, bst, bst + B_HALF);
             if (wt == 0) sm.Bmask[sb] = mask;
             if (!(dbg & 128)) tc::fence_proxy_async_smem();
-            tc::mbar_arrive(&sm.b_full[sb]);
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sm.b_full[sb]);
             TPROF_END(1);
         }
     }

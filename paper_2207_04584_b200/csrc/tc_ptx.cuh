@@ -55,6 +55,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra WAIT_%=;\n\t"
         "}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+#elif defined(HG_MBAR_NOHINT)
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t"
+        "}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 #else
     asm volatile(
         "{\n\t"
@@ -64,6 +72,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n\t"
         "}\n" :: "r"(smem_u32(bar)), "r"(parity), "n"(HG_MBAR_SUSPEND_NS) : "memory");
 #endif
+}
+// Spin on the non-blocking test: for the single-warp roles on the critical hand-off chain
+// (MMA issuers, loaders), where wake-up latency matters more than the issue slots
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t"
+        "}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 // Kept for the roles that usually run ahead (same wait; the hint already suspends).
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
