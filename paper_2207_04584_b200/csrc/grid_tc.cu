@@ -101,7 +101,10 @@ constexpr uint32_t TC_CPB_SPARSE = 80;
 constexpr unsigned TC_PW_MIN_CBLOCKS = 4;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t D_COLS = TC_NB * TC_N;      // one accumulator buffer: 12 blocks x 16 columns
-constexpr uint32_t A_COL0 = 2 * D_COLS;        // 384: A stages after the two D buffers
+#ifndef HG_TC_ND
+#define HG_TC_ND 2
+#endif
+constexpr uint32_t A_COL0 = HG_TC_ND * D_COLS;  // 384: A stages after the two D buffers
 static_assert(A_COL0 + NA * 64 <= TMEM_COLS, "TMEM budget");
 static_assert(SEG_DENSE > NA && SEG_SPARSE > NA, "a segment is promoted NA chunks into the next one");
 // B stage layout (per hi / lo half): K-major, 128-byte swizzle.  Row R = 16 q + n (slot q,
@@ -713,7 +716,12 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                                                 tc::idesc_tf32(TC_M, TC_N * r));
                 }
             }
-            tc::mma_commit_warp(&sm.done[c % NBF]);    // a commit costs ~100 cycles: one per chunk
+            if (dbg & 4096) {                          // debug (with no MMAs): plain arrive
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&sm.done[c % NBF]);
+            } else {
+                tc::mma_commit_warp(&sm.done[c % NBF]);    // a commit costs ~100 cycles: one per chunk
+            }
             if (c % SEG == SEG - 1 || c == nchunks - 1) tc::mma_commit_warp(&sm.seg_done[d]);
             __syncwarp();
             TPROF_END(2);

@@ -281,3 +281,26 @@ def test_launches_are_counted():
     with Plan(lon, lat, w.map, w.fwhm_deg) as p:
         p.grid(vals)
     assert b.hegrid_launch_count() > before
+
+
+def test_tc_pw_cta_order_invariant(monkeypatch):
+    """The precomputed-weight engine's result does not depend on the CTA walk (channel-block
+    groups, super-tiles): every (tile, channel block) is computed the same way wherever it
+    runs, so the maps are bit-identical."""
+    w = small_workload("cfg2", n=160 * 120, tracks=160, per_track=120, nx=45, ny=41,
+                       field_lon=0.8, field_lat=0.75, channels=700)
+    lon, lat, vals = make_inputs(w)
+    monkeypatch.setenv("HEGRID_TC_PW", "1")
+    outs = []
+    for group, sup in (("1", "1"), ("3", "2"), ("6", "4")):
+        monkeypatch.setenv("HEGRID_TC_GROUP", group)
+        monkeypatch.setenv("HEGRID_TC_SUPER", sup)
+        with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, engine="tc") as p:
+            d = vals.cuda()
+            out, W = p.grid(d)
+            outs.append((out.cpu().numpy(), W.cpu().numpy()))
+    for o, W in outs[1:]:
+        np.testing.assert_array_equal(o, outs[0][0])
+        np.testing.assert_array_equal(W, outs[0][1])
+    o, Wo, _ = oracle_grid(w, lon, lat, vals)
+    compare(outs[0][0].reshape(700, -1), outs[0][1].reshape(-1), o, Wo)
