@@ -514,6 +514,9 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
 // 0 total, 1 issuer wait A, 2 issuer wait B, 3 A wait V, 4 A wait A-empty, 5 B wait B-empty,
 // 6 V wait V-empty, 7 B work, 8 A work, 9 epilogue, 10 issuer issue
 __device__ unsigned long long g_tc_prof[16];
+// Timeline of one CTA (profiling builds, HEGRID_TC_DEBUG bit 8192): clock64 per (chunk, event)
+__device__ long long g_tl[256][12];
+#define TL(ev, c) do { if (tl_on && (c) < 256) g_tl[(c)][(ev)] = clock64(); } while (0)
 
 // ------------------------------------------------------------------ the kernel
 template <int SEG, bool PW>
@@ -542,6 +545,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     constexpr bool prof = false;
     (void)dbg_in;
 #endif
+    const bool tl_on = prof && (dbg & 8192) && blockIdx.x == 1000;
     const long long t_start = clock64();
     unsigned long long pw[4] = {0, 0, 0, 0};
 #define TPROF_BEGIN long long _t0 = prof ? clock64() : 0
@@ -686,11 +690,13 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 HG_WAIT_CRIT(&sm.a_full[sa], (c / NA) & 1);
                 TPROF_END(0);
             }
+            if (issuer == 0 && lane == 0) TL(3, c);
             {
                 TPROF_BEGIN;
                 HG_WAIT_CRIT(&sm.b_full[sb], PW ? (c / NBF) & 1 : (c / NBS) & 1);
                 TPROF_END(1);
             }
+            if (issuer == 0 && lane == 0) TL(4, c);
             tc::fence_after_sync();
             const uint32_t mask = sm.Bmask[sb];
             // B operand: OTF = weight stage sb (lo half at B_HALF); PW = the entry's ring bytes
@@ -723,6 +729,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 tc::mma_commit_warp(&sm.done[c % NBF]);    // a commit costs ~100 cycles: one per chunk
             }
             if (c % SEG == SEG - 1 || c == nchunks - 1) tc::mma_commit_warp(&sm.seg_done[d]);
+            if (issuer == 0 && lane == 0) TL(5, c);
             __syncwarp();
             TPROF_END(2);
         };
@@ -784,6 +791,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     tc::mbar_arrive(&sm.v_full[sv]);
                 } else {
                     // the geometry feeds the on-the-fly B producers only
+                    TL(0, c);
                     tc::mbar_arrive_expect_tx(&sm.v_full[sv], (uint32_t)V_STAGE + (PW ? 0u : nk * 16));
                     tc::tma_load_2d(&sm.Vs[sv][0], &tmap_v, cb, (int)e.x, &sm.v_full[sv]);
                     if (!PW) tc::bulk_g2s(&sm.Gs[sv][0], pd.geo + e.x, nk * 16, &sm.v_full[sv]);
@@ -851,6 +859,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     if (dbg & 512) {
                         tc::mbar_arrive(&sm.b_full[k]);
                     } else {
+                        TL(7, c);
                         tc::mbar_arrive_expect_tx(&sm.b_full[k], bytes);
                         tc::bulk_g2s(&sm.B[off], wimg + (size_t)sc[u] * (2u * SLOT_BYTES), bytes, &sm.b_full[k]);
                     }
@@ -889,6 +898,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 tc::mbar_wait(&sm.v_full[sv], (c / NV) & 1);
                 TPROF_END(0);
             }
+            if (warp == 4 && lane == 0) TL(1, c);
             const float* vs = reinterpret_cast<const float*>(&sm.Vs[sv][0]) + k0 * TC_M + chl;
             const uint4 ee = sm.Es[sv];
             const uint32_t nk = ee.y & 63;
@@ -913,6 +923,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             uint32_t dep = ee.x ^ ee.y ^ ee.z;
 #pragma unroll
             for (int k = 0; k < KPW; ++k) dep ^= lo[k] ^ hi[k];
+            if (warp == 4 && lane == 0 && tl_on && c < 256) g_tl[c][8] = clock64() + (dep == 0x12345u);
             asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[warp])), "r"(dep) : "memory");
             // one arrive per warp (hundreds of per-thread arrives on one mbarrier serialise)
             __syncwarp();
@@ -925,9 +936,11 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 if (c >= NA) tc::mbar_wait(&sm.done[(c - NA) % NBF], ((c - NA) / NBF) & 1);
                 TPROF_END(1);
             }
+            if (warp == 4 && lane == 0 && c >= NA) TL(6, c - NA);
             tc::fence_after_sync();
             const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + A_COL0 + sa * 64 + k0;
-            if (dbg & 256) {
+            if (warp == 4 && lane == 0) TL(10, c);
+            if (dbg & (256 | 16384)) {
             } else if constexpr (KPW == 32) {
                 tc::tmem_st32(ta, hi);
                 tc::tmem_st32(ta + 32, lo);
@@ -947,9 +960,11 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 TPROF_END(3);
             }
             tc::wait_st();
+            if (warp == 4 && lane == 0) TL(9, c);
             tc::fence_before_sync();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&sm.a_full[c % NA]);
+            if (warp == 4 && lane == 0) TL(2, c);
             if (c + 1 < nchunks) {
                 const int cn = c + 1;
                 if (cn >= SEG && cn % SEG == NA) {
@@ -1168,6 +1183,15 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
                 (double)p->tc_stats[4] / p->tc_stats[0]);
         unsigned long long z[16] = {0};
         cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
+        if (dbg & 8192) {
+            static long long tl[256][12];
+            cudaMemcpyFromSymbol(tl, g_tl, sizeof(tl));
+            const long long t0 = tl[40][0];
+            fprintf(stderr, "[tc tl] chunk: vTMA Avfull Asplit Awaitst Aafull Astore | Igota Igotb Icommit Adone Wcopy (cycles rel. to chunk 40 vTMA)\n");
+            for (int c = 40; c < 60; ++c)
+                fprintf(stderr, "[tc tl] %3d: %7lld %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld\n", c, tl[c][0] - t0, tl[c][1] - t0,
+                        tl[c][8] - t0, tl[c][9] - t0, tl[c][2] - t0, tl[c][10] - t0, tl[c][3] - t0, tl[c][4] - t0, tl[c][5] - t0, tl[c][6] - t0, tl[c][7] - t0);
+        }
     }
     return cuda_status(cudaGetLastError());
 }
