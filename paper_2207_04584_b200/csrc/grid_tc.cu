@@ -65,7 +65,13 @@ constexpr int TC_BX = 4, TC_BY = HG_TC_BY; // blocks per CTA tile (16 x 4 TC_BY 
 constexpr int TC_NB = TC_BX * TC_BY;      // 12 blocks
 constexpr int TC_N = 16;                  // cells per block: 4 x 4
 constexpr int TC_TW = TC_BX * 4, TC_TH = TC_BY * 4;
-constexpr int TC_KC = 32;                 // samples per chunk (4 MMA K-steps of 8)
+#ifndef HG_TC_KC
+#define HG_TC_KC 32
+#endif
+constexpr int TC_KC = HG_TC_KC;           // samples per chunk (TC_KC / 8 MMA K-steps)
+constexpr int KA = TC_KC / 32;            // 128-B swizzle atoms along K (32 tf32 each)
+constexpr int LKA = KA == 2 ? 1 : 0;
+static_assert(TC_KC == 32 || TC_KC == 64, "chunks of 32 or 64 samples");
 #ifndef HG_TC_NA
 #define HG_TC_NA 2
 #endif
@@ -96,7 +102,7 @@ constexpr int MAXQ = 8;                   // max blocks (B slots) per chunk entr
 constexpr int SEG_DENSE = HG_TC_SEG, SEG_SPARSE = HG_TC_SEG_SPARSE;
 // A block touched by at most this many chunks in the whole tile accumulates few enough MMAs
 // per segment at SEG_SPARSE (measured: max rel err 4e-6 at cfg4, where the max is 70)
-constexpr uint32_t TC_CPB_SPARSE = 80;
+constexpr uint32_t TC_CPB_SPARSE = 80 / KA;
 // PW mode (precomputed weight image) from this many 128-channel blocks per launch
 constexpr unsigned TC_PW_MIN_CBLOCKS = 4;
 constexpr uint32_t TMEM_COLS = 512;
@@ -105,15 +111,16 @@ constexpr uint32_t D_COLS = TC_NB * TC_N;      // one accumulator buffer: 12 blo
 #define HG_TC_ND 2
 #endif
 constexpr uint32_t A_COL0 = HG_TC_ND * D_COLS;  // 384: A stages after the two D buffers
-static_assert(A_COL0 + NA * 64 <= TMEM_COLS, "TMEM budget");
+static_assert(A_COL0 + NA * 2 * TC_KC <= TMEM_COLS, "TMEM budget");
 static_assert(SEG_DENSE > NA && SEG_SPARSE > NA, "a segment is promoted NA chunks into the next one");
 // B stage layout (per hi / lo half): K-major, 128-byte swizzle.  Row R = 16 q + n (slot q,
 // cell n) holds the chunk's 32 tf32 weights (128 B); 8-row groups are 1024-B swizzle atoms
 // (SBO = 1024); the 16-B k-quad j of row R sits at chunk position j ^ (R & 7), so the 32
 // lanes of a producer warp storing one k-quad each hit 8 distinct bank groups (no
 // conflicts); the MMA K-step ks starts 32 B further into the atom.
-constexpr uint32_t B_ROW = TC_KC * 4;                // 128 B
-constexpr uint32_t B_HALF = MAXQ * TC_N * B_ROW;     // 16 KB
+constexpr uint32_t B_ROW = 128;                      // one swizzle-atom row: 32 tf32
+constexpr uint32_t ATOM_SLOT = TC_N * B_ROW;         // 2 KB: one block's 16 cells x 32 samples
+constexpr uint32_t B_HALF = MAXQ * KA * ATOM_SLOT;   // 16 KB (32-sample chunks)
 constexpr uint32_t B_STAGE = 2 * B_HALF;             // 32 KB (hi + lo)
 constexpr int V_ROW = TC_M * 4;                      // 512 B
 constexpr int V_STAGE = TC_KC * V_ROW;               // 16 KB
@@ -125,8 +132,12 @@ constexpr int NBF = 16;
 // PW mode (precomputed weight image): the weights of a schedule entry (nq in-reach blocks) are
 // nq x 2 KB of tf32 hi then nq x 2 KB of lo, already in the operand layout; one bulk copy per
 // entry into a byte ring in shared memory (entries placed contiguously, wrapping to 0).
-constexpr uint32_t SLOT_BYTES = TC_N * B_ROW;        // 2 KB: one block's 16 cells x 32 samples
-constexpr uint32_t RING = 76 * 1024;
+constexpr uint32_t SLOT_BYTES = KA * ATOM_SLOT;      // one block, one half (hi or lo): 2 KB at K = 32
+#ifndef HG_TC_RING_KB
+#define HG_TC_RING_KB 76
+#endif
+constexpr uint32_t RING = HG_TC_RING_KB * 1024;
+static_assert(RING >= MAXQ * 2 * SLOT_BYTES, "the ring holds the largest entry");
 constexpr uint32_t REGION0 = RING > NBS * B_STAGE ? RING : NBS * B_STAGE;
 
 struct TcSmem {
@@ -149,10 +160,12 @@ struct TcSmem {
 static_assert(offsetof(TcSmem, B) == 0 && offsetof(TcSmem, Vs) % 1024 == 0, "stage layout");
 static_assert(sizeof(TcSmem) + 1024 <= 232448, "shared memory budget");
 
-// byte offset of (slot q, cell n, sample k) inside one half (hi or lo) of a B stage
-__device__ __forceinline__ uint32_t b_off(int q, int n, int kq) {
-    const int r = q * TC_N + n;
-    return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((kq ^ (r & 7)) << 4));
+// byte offset of (slot q, cell n, sample quad kq) inside one half (hi or lo) of an operand
+// with ns slots: K-atom a = kq / 8 holds the ns slots' 16-row groups of that atom
+// ([atom][slot][16 rows x 128 B]), so the rows of consecutive slots stay 1024 B per 8 apart
+__device__ __forceinline__ uint32_t b_off(int q, int n, int kq, int ns) {
+    const int r = q * TC_N + n, a = kq >> 3, k8 = kq & 7;
+    return (uint32_t)(a * ns * (int)ATOM_SLOT + (r >> 3) * 1024 + (r & 7) * 128 + ((k8 ^ (r & 7)) << 4));
 }
 
 // The B operand of one chunk entry: thread wt (0..255) of the B-producer group computes its
@@ -163,10 +176,11 @@ __device__ __forceinline__ uint32_t b_off(int q, int n, int kq) {
 __device__ __forceinline__ void entry_weights(const Geom& g, const PlanDev& pd, int i0, int j0,
                                               int wt, const float (&cosr)[TC_BY],
                                               const float4 (&g4)[4], uint32_t pstart, int row,
-                                              uint32_t blist, int nq, uint8_t* hi, uint8_t* lo) {
-    const int kq = wt & 7, ch2 = (wt >> 3) & 1, rr = (wt >> 4) & 3, q0 = wt >> 6;
+                                              uint32_t blist, int nq, int ns, uint8_t* hi, uint8_t* lo) {
+    const int kq = wt & (8 * KA - 1), ch2 = (wt >> (3 + LKA)) & 1, rr = (wt >> (4 + LKA)) & 3;
+    const int q0 = wt >> (6 + LKA);
 #pragma unroll 1
-    for (int q = q0; q < nq; q += 4) {
+    for (int q = q0; q < nq; q += 4 / KA) {
         const int b = (blist >> (4 * q)) & 15;
         const int by = b / TC_BX;
         const int cj = j0 + by * 4 + rr;
@@ -191,7 +205,7 @@ __device__ __forceinline__ void entry_weights(const Geom& g, const PlanDev& pd, 
             tc::split_tf32(w[1][cc], h4.y, l4.y);
             tc::split_tf32(w[2][cc], h4.z, l4.z);
             tc::split_tf32(w[3][cc], h4.w, l4.w);
-            const uint32_t o = b_off(q, n, kq);
+            const uint32_t o = b_off(q, n, kq, ns);
             *reinterpret_cast<uint4*>(hi + o) = h4;
             *reinterpret_cast<uint4*>(lo + o) = l4;
         }
@@ -201,7 +215,7 @@ __device__ __forceinline__ void entry_weights(const Geom& g, const PlanDev& pd, 
 // cos(lat) of the cell rows a B-producer thread can touch (rr = its row within a block)
 __device__ __forceinline__ void entry_cos_rows(const Geom& g, const PlanDev& pd, int j0, int wt,
                                                float (&cosr)[TC_BY]) {
-    const int rr = (wt >> 4) & 3;
+    const int rr = (wt >> (4 + LKA)) & 3;
 #pragma unroll
     for (int by = 0; by < TC_BY; ++by) {
         const int cj = j0 + by * 4 + rr;
@@ -230,7 +244,7 @@ __device__ __forceinline__ bool block_reachable(const Geom& g, int bi, int bj, d
 }
 
 // Chunk schedule: one warp per tile; lanes evaluate 32 consecutive chunks of a row at once.
-// Entry = {plan position, n | bin row << 6, block mask, block list (4-bit nibbles, mask order)}.
+// Entry = {plan position, n | bin row << 8, block mask, block list (4-bit nibbles, mask order)}.
 // n_out != nullptr: count only; otherwise write entries at off[tile].
 __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int tiles,
                               uint32_t* __restrict__ n_out, const uint32_t* __restrict__ off,
@@ -305,7 +319,7 @@ __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int ti
                         part |= rest & (~rest + 1u);
                         rest &= rest - 1;
                     }
-                    sched[pos++] = make_uint4(p, n | ((uint32_t)br << 6), part, list);
+                    sched[pos++] = make_uint4(p, n | ((uint32_t)br << 8), part, list);
                 }
             }
             cnt += tot;
@@ -364,12 +378,12 @@ k_tc_wimage(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict_
             uint8_t* __restrict__ wimg) {
     const int tiles_x = (g.nx + TC_TW - 1) / TC_TW;
     const int i0 = (blockIdx.x % tiles_x) * TC_TW, j0 = (blockIdx.x / tiles_x) * TC_TH;
-    const int wt = threadIdx.x, kq = wt & 7;
+    const int wt = threadIdx.x, kq = wt & (8 * KA - 1);
     float cosr[TC_BY];
     entry_cos_rows(g, pd, j0, wt, cosr);
     for (uint32_t ei = tile_off[blockIdx.x]; ei < tile_off[blockIdx.x + 1]; ++ei) {
         const uint4 e = __ldg(&sched[ei]);
-        const uint32_t pstart = e.x, nk = e.y & 63;
+        const uint32_t pstart = e.x, nk = e.y & 255;
         const int nq = __popc(e.z);
         float4 g4[4];
 #pragma unroll
@@ -377,7 +391,7 @@ k_tc_wimage(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict_
             g4[u] = (uint32_t)(4 * kq + u) < nk ? __ldg(&pd.geo[pstart + 4 * kq + u])
                                                 : make_float4(0.0f, kInvalidDy, 0.0f, 0.0f);
         uint8_t* hi = wimg + (size_t)__ldg(&wslot[ei]) * (2u * SLOT_BYTES);
-        entry_weights(g, pd, i0, j0, wt, cosr, g4, pstart, (int)(e.y >> 6), e.w, nq, hi,
+        entry_weights(g, pd, i0, j0, wt, cosr, g4, pstart, (int)(e.y >> 8), e.w, nq, nq, hi,
                       hi + (size_t)nq * SLOT_BYTES);
     }
 }
@@ -702,14 +716,15 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             // B operand: OTF = weight stage sb (lo half at B_HALF); PW = the entry's ring bytes
             // (nq slots of hi, then nq slots of lo)
             const uint32_t b_addr = PW ? tc::smem_u32(&sm.B[sm.Boff[sb]]) : tc::smem_u32(&sm.B[sb * B_STAGE]);
-            const uint64_t lo16 = PW ? (uint64_t)((__popc(mask) * SLOT_BYTES) >> 4) : (uint64_t)(B_HALF >> 4);
+            const int ns = PW ? __popc(mask) : MAXQ;       // slots of the B operand's layout
+            const uint64_t lo16 = (uint64_t)((ns * SLOT_BYTES) >> 4);
             TPROF_BEGIN;
             if (!(dbg & 2)) {
                 // runs of consecutive in-reach blocks = consecutive B slots (slots follow the
                 // mask order); D buffers are zeroed before each segment, so every MMA
                 // accumulates.  Each run is 12 MMAs behind one elect.
                 const uint32_t dh0 = tc::sdesc_sw128_lo(b_addr);
-                const uint32_t a0 = tmem + A_COL0 + sa * 64;
+                const uint32_t a0 = tmem + A_COL0 + sa * 2 * TC_KC;
                 const uint32_t dbase = tmem + (uint32_t)d * D_COLS;
                 uint32_t mm = mask & rows;
                 while (mm) {
@@ -717,9 +732,12 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     const int r = __ffs(~(mm >> b)) - 1;
                     mm &= ~(((1u << r) - 1u) << b);
                     const int q = __popc(mask & ((1u << b) - 1u));     // B slot of block b
-                    const uint32_t bh = dh0 + (uint32_t)((q * SLOT_BYTES) >> 4);
-                    tc::mma12_3xtf32<(32 >> 4)>(dbase + (uint32_t)(b * TC_N), a0, bh, bh + (uint32_t)lo16,
-                                                tc::idesc_tf32(TC_M, TC_N * r));
+#pragma unroll
+                    for (int a = 0; a < KA; ++a) {    // K-atom a: K-steps 4a .. 4a + 3
+                        const uint32_t bh = dh0 + (uint32_t)(((a * ns + q) * ATOM_SLOT) >> 4);
+                        tc::mma12_3xtf32<(32 >> 4), TC_KC>(dbase + (uint32_t)(b * TC_N), a0 + 32 * a, bh,
+                                                           bh + (uint32_t)lo16, tc::idesc_tf32(TC_M, TC_N * r));
+                    }
                 }
             }
             if (dbg & 4096) {                          // debug (with no MMAs): plain arrive
@@ -776,7 +794,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const int cp = c + PF;
             const uint32_t xp = __shfl_sync(0xffffffffu, (cp >> 5) == (c >> 5) ? cur.x : nxt.x, cp & 31);
             if (lane == 0) {
-                const uint32_t nk = e.y & 63;
+                const uint32_t nk = e.y & 255;
                 const int sv = c % NV;
 #ifndef HG_TC_NO_VPF
                 if (cp < nchunks) tc::tma_prefetch_2d(&tmap_v, cb, (int)xp);
@@ -901,7 +919,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             if (warp == 4 && lane == 0) TL(1, c);
             const float* vs = reinterpret_cast<const float*>(&sm.Vs[sv][0]) + k0 * TC_M + chl;
             const uint4 ee = sm.Es[sv];
-            const uint32_t nk = ee.y & 63;
+            const uint32_t nk = ee.y & 255;
             if ((c / SEG) & 1) segmask1 |= ee.z; else segmask0 |= ee.z;
             if (dbg & 256) {                        // debug: no value work
 #pragma unroll
@@ -938,15 +956,20 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             }
             if (warp == 4 && lane == 0 && c >= NA) TL(6, c - NA);
             tc::fence_after_sync();
-            const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + A_COL0 + sa * 64 + k0;
+            const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + A_COL0 + sa * 2 * TC_KC + k0;
             if (warp == 4 && lane == 0) TL(10, c);
             if (dbg & (256 | 16384)) {
+            } else if constexpr (KPW == 64) {
+                tc::tmem_st32p(ta, hi);
+                tc::tmem_st32p(ta + 32, hi + 32);
+                tc::tmem_st32p(ta + TC_KC, lo);
+                tc::tmem_st32p(ta + TC_KC + 32, lo + 32);
             } else if constexpr (KPW == 32) {
                 tc::tmem_st32(ta, hi);
-                tc::tmem_st32(ta + 32, lo);
+                tc::tmem_st32(ta + TC_KC, lo);
             } else {
                 tc::tmem_st16(ta, hi);
-                tc::tmem_st16(ta + 32, lo);
+                tc::tmem_st16(ta + TC_KC, lo);
             }
         };
         if (nchunks > 0) {
@@ -990,7 +1013,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         // (on-the-fly mode only) item = (slot q, cell row rr, column pair ch2, sample quad
         // kq): 4 samples x 2 cells; a thread keeps (kq, ch2, rr) and takes slots q0, q0 + 4
         const int wt = tid - 8 * 32;                  // 0..255
-        const int kq = wt & 7;
+        const int kq = wt & (8 * KA - 1);
         float cosr[TC_BY];
         entry_cos_rows(g, pd, j0, wt, cosr);
         for (int c = 0; c < nchunks; ++c) {
@@ -1002,8 +1025,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 TPROF_END(2);
             }
             const uint4 e = sm.Es[sv];
-            const uint32_t pstart = e.x, nk = e.y & 63, mask = e.z, blist = e.w;
-            const int row = (int)(e.y >> 6);
+            const uint32_t pstart = e.x, nk = e.y & 255, mask = e.z, blist = e.w;
+            const int row = (int)(e.y >> 8);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 g4[u] = sm.Gs[sv][4 * kq + u];
@@ -1032,7 +1055,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             TPROF_BEGIN;
             const int nq = (dbg & 1) ? 0 : __popc(mask);
             uint8_t* bst = &sm.B[sb * B_STAGE];
-            entry_weights(g, pd, i0, j0, wt, cosr, g4, pstart, row, blist, nq, bst, bst + B_HALF);
+            entry_weights(g, pd, i0, j0, wt, cosr, g4, pstart, row, blist, nq, MAXQ, bst, bst + B_HALF);
             if (wt == 0) sm.Bmask[sb] = mask;
             if (!(dbg & 128)) tc::fence_proxy_async_smem();
             __syncwarp();

@@ -193,10 +193,10 @@ __device__ __forceinline__ void mma_run_3xtf32(uint32_t d, uint32_t a0, uint64_t
 // K-step advancing the start address by KS_STEP (16-B units).  Each base value is moved to a
 // uniform register once per run instead of once per MMA.
 constexpr uint32_t kDescHiSw128 = 0x40004040u;   // layout 2 << 61 | version << 46 | (1024 >> 4) << 32
-template <int KS_STEP>
+template <int KS_STEP, int ALO = 32>
 __device__ __forceinline__ void mma12_3xtf32(uint32_t d, uint32_t a0, uint32_t bh_lo, uint32_t bl_lo,
                                              uint32_t idesc) {
-#define HG_MMA12_KS(ks, bh, bl, ah, al)                                                  \
+#define HG_MMA12_KS(bh, bl, ah, al)                                                      \
     "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+" #ah "], " #bh ", %4, 1;\n\t"       \
     "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+" #ah "], " #bl ", %4, 1;\n\t"       \
     "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+" #al "], " #bh ", %4, 1;\n\t"
@@ -220,10 +220,11 @@ __device__ __forceinline__ void mma12_3xtf32(uint32_t d, uint32_t a0, uint32_t b
         "mov.b64 l2, {y2, %8};\n\t"
         "mov.b64 l3, {y3, %8};\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
-        HG_MMA12_KS(0, h0, l0, 0, 32) HG_MMA12_KS(1, h1, l1, 8, 40)
-        HG_MMA12_KS(2, h2, l2, 16, 48) HG_MMA12_KS(3, h3, l3, 24, 56)
+        HG_MMA12_KS(h0, l0, 0, %9) HG_MMA12_KS(h1, l1, 8, %10)
+        HG_MMA12_KS(h2, l2, 16, %11) HG_MMA12_KS(h3, l3, 24, %12)
         "}\n" :: "r"(d), "r"(a0), "r"(bh_lo), "r"(bl_lo), "r"(idesc), "n"(KS_STEP),
-        "n"(2 * KS_STEP), "n"(3 * KS_STEP), "n"(kDescHiSw128) : "memory");
+        "n"(2 * KS_STEP), "n"(3 * KS_STEP), "n"(kDescHiSw128), "n"(ALO), "n"(ALO + 8),
+        "n"(ALO + 16), "n"(ALO + 24) : "memory");
 #undef HG_MMA12_KS
 }
 // low word of a K-major SWIZZLE_128B descriptor (start address >> 4, LBO field 1)
@@ -280,6 +281,17 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
 
 // ---- TMEM <-> registers (32 lanes x 32 bit, per warp) ------------------------------
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, "
+        "%10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, "
+        "%27, %28, %29, %30, %31, %32};"
+        :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),
+           "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]),
+           "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]),
+           "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+           "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) : "memory");
+}
+__device__ __forceinline__ void tmem_st32p(uint32_t taddr, const uint32_t* r) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, "
         "%10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, "
