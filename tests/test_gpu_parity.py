@@ -304,3 +304,26 @@ def test_tc_pw_cta_order_invariant(monkeypatch):
         np.testing.assert_array_equal(W, outs[0][1])
     o, Wo, _ = oracle_grid(w, lon, lat, vals)
     compare(outs[0][0].reshape(700, -1), outs[0][1].reshape(-1), o, Wo)
+
+
+def test_tc_pw_and_otf_bit_identical(monkeypatch):
+    """The precomputed weight image holds exactly the weights the on-the-fly producers
+    compute, and both modes accumulate each block in the same chunk order: the maps are
+    bit-identical whichever mode a launch takes (the host path mixes them when its last
+    channel block is small)."""
+    w = small_workload("cfg2", n=150 * 110, tracks=150, per_track=110, nx=38, ny=35,
+                       field_lon=0.7, field_lat=0.65, channels=530)
+    lon, lat, vals = make_inputs(w)
+    res = []
+    for pw in ("0", "1"):
+        monkeypatch.setenv("HEGRID_TC_PW", pw)
+        with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, engine="tc") as p:
+            out, W = p.grid(vals.cuda())
+            res.append((out.cpu().numpy(), W.cpu().numpy()))
+    np.testing.assert_array_equal(res[0][0], res[1][0])
+    np.testing.assert_array_equal(res[0][1], res[1][1])
+    # host path: 512-channel blocks (precomputed weights) plus an 18-channel tail block
+    monkeypatch.delenv("HEGRID_TC_PW")
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, engine="tc", channel_block=512) as p:
+        out_h, W_h = p.grid(vals.numpy())
+    np.testing.assert_array_equal(np.asarray(out_h).reshape(res[0][0].shape), res[0][0])
