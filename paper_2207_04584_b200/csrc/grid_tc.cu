@@ -549,7 +549,10 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     // B producers otherwise); each lane quarter's chunk columns are split between its warps
     constexpr int A_WARPS = PW ? 8 : 4, A_GROUPS = A_WARPS / 4, A_THREADS = 32 * A_WARPS;
     constexpr int KPW = TC_KC / A_GROUPS;
-    constexpr int NI = PW ? (TC_BY < 3 ? TC_BY : 3) : 2;   // MMA issuer warps
+#ifndef HG_TC_NI_PW
+#define HG_TC_NI_PW 3
+#endif
+    constexpr int NI = PW ? (TC_BY < HG_TC_NI_PW ? TC_BY : HG_TC_NI_PW) : 2;   // MMA issuer warps
 #ifdef HG_TC_PROF
     // debug switches (HEGRID_TC_DEBUG) and cycle counters: only in profiling builds
     const int dbg = dbg_in;
@@ -676,7 +679,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     // sub-partitions) issues the MMAs of the tile's block rows r with r % NI == i, so the
     // per-MMA issue cost is spread over NI instruction streams.  Each D column block is always
     // fed by the same issuer in chunk order: the accumulation order stays fixed.
-    const int issuer = warp == 0 ? 0 : warp == 3 ? 1 : (NI > 2 && warp == 13) ? 2 : -1;
+    const int issuer = warp == 0 ? 0 : (NI > 1 && warp == 3) ? 1 : (NI > 2 && warp == 13) ? 2 : -1;
     if (issuer >= 0) {
         // ============================ MMA issuer =============================
         // chunk c uses A stage c % NA; the loop is unrolled by NA so the stage (and with it
@@ -727,6 +730,29 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 const uint32_t a0 = tmem + A_COL0 + sa * 2 * TC_KC;
                 const uint32_t dbase = tmem + (uint32_t)d * D_COLS;
                 uint32_t mm = mask & rows;
+#if defined(HG_TC_MMA36)
+                static_assert(KA == 1, "36-MMA issue for 32-sample chunks");
+                while (mm) {                       // up to three runs per asm block
+                    uint32_t dd[3] = {0, 0, 0}, bb[3] = {0, 0, 0}, ii[3] = {0, 0, 0};
+                    int nr = 0;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        if (mm) {
+                            const int b = __ffs(mm) - 1;
+                            const int r = __ffs(~(mm >> b)) - 1;
+                            mm &= ~(((1u << r) - 1u) << b);
+                            const int q = __popc(mask & ((1u << b) - 1u));
+                            dd[k] = dbase + (uint32_t)(b * TC_N);
+                            bb[k] = dh0 + (uint32_t)((q * ATOM_SLOT) >> 4);
+                            ii[k] = tc::idesc_tf32(TC_M, TC_N * r);
+                            nr = k + 1;
+                        }
+                    }
+                    tc::mma36_3xtf32<(32 >> 4), TC_KC>(a0, dd[0], bb[0], bb[0] + (uint32_t)lo16, ii[0],
+                                                       dd[1], bb[1], bb[1] + (uint32_t)lo16, ii[1],
+                                                       dd[2], bb[2], bb[2] + (uint32_t)lo16, ii[2], nr);
+                }
+#else
                 while (mm) {
                     const int b = __ffs(mm) - 1;
                     const int r = __ffs(~(mm >> b)) - 1;
@@ -739,6 +765,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                                                            bh + (uint32_t)lo16, tc::idesc_tf32(TC_M, TC_N * r));
                     }
                 }
+#endif
             }
             if (dbg & 4096) {                          // debug (with no MMAs): plain arrive
                 __syncwarp();

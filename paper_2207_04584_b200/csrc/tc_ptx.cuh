@@ -227,6 +227,53 @@ __device__ __forceinline__ void mma12_3xtf32(uint32_t d, uint32_t a0, uint32_t b
         "n"(ALO + 16), "n"(ALO + 24) : "memory");
 #undef HG_MMA12_KS
 }
+// Up to three runs of one chunk (4 K-steps x 3 products each, 36 MMAs) behind one elect:
+// runs 1 and 2 are predicated on nr > 1, nr > 2.  Every operand base enters the asm once
+// (D, B-descriptor low words, instruction descriptor per run; one A base), so ptxas moves
+// each to a uniform register once per chunk instead of once per MMA.
+template <int KS_STEP, int ALO = 32>
+__device__ __forceinline__ void mma36_3xtf32(uint32_t a0, uint32_t d0, uint32_t bh0, uint32_t bl0,
+                                             uint32_t i0, uint32_t d1, uint32_t bh1, uint32_t bl1,
+                                             uint32_t i1, uint32_t d2, uint32_t bh2, uint32_t bl2,
+                                             uint32_t i2, int nr) {
+#define HG_MMA36_RUN(P, D, BH, BL, ID)                                                         \
+    "add.u32 x1, " BH ", %13;\n\t" "add.u32 x2, " BH ", %14;\n\t" "add.u32 x3, " BH ", %15;\n\t" \
+    "add.u32 y1, " BL ", %13;\n\t" "add.u32 y2, " BL ", %14;\n\t" "add.u32 y3, " BL ", %15;\n\t" \
+    "mov.b64 h0, {" BH ", %16};\n\t" "mov.b64 h1, {x1, %16};\n\t"                              \
+    "mov.b64 h2, {x2, %16};\n\t" "mov.b64 h3, {x3, %16};\n\t"                                  \
+    "mov.b64 l0, {" BL ", %16};\n\t" "mov.b64 l1, {y1, %16};\n\t"                              \
+    "mov.b64 l2, {y2, %16};\n\t" "mov.b64 l3, {y3, %16};\n\t"                                  \
+    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0], h0, " ID ", 1;\n\t"                 \
+    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0], l0, " ID ", 1;\n\t"                 \
+    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+%17], h0, " ID ", 1;\n\t"             \
+    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+8], h1, " ID ", 1;\n\t"               \
+    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+8], l1, " ID ", 1;\n\t"               \
+    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+%18], h1, " ID ", 1;\n\t"             \
+    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+16], h2, " ID ", 1;\n\t"              \
+    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+16], l2, " ID ", 1;\n\t"              \
+    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+%19], h2, " ID ", 1;\n\t"             \
+    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+24], h3, " ID ", 1;\n\t"              \
+    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+24], l3, " ID ", 1;\n\t"              \
+    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+%20], h3, " ID ", 1;\n\t"
+    asm volatile(
+        "{\n\t"
+        ".reg .pred e, e1, e2, q1, q2;\n\t"
+        ".reg .b32 x1, x2, x3, y1, y2, y3;\n\t"
+        ".reg .b64 h0, h1, h2, h3, l0, l1, l2, l3;\n\t"
+        "setp.gt.s32 q1, %21, 1;\n\t"
+        "setp.gt.s32 q2, %21, 2;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "and.pred e1, e, q1;\n\t"
+        "and.pred e2, e, q2;\n\t"
+        HG_MMA36_RUN("e", "%1", "%2", "%3", "%4")
+        HG_MMA36_RUN("e1", "%5", "%6", "%7", "%8")
+        HG_MMA36_RUN("e2", "%9", "%10", "%11", "%12")
+        "}\n" :: "r"(a0), "r"(d0), "r"(bh0), "r"(bl0), "r"(i0), "r"(d1), "r"(bh1), "r"(bl1),
+        "r"(i1), "r"(d2), "r"(bh2), "r"(bl2), "r"(i2), "n"(KS_STEP), "n"(2 * KS_STEP),
+        "n"(3 * KS_STEP), "n"(kDescHiSw128), "n"(ALO), "n"(ALO + 8), "n"(ALO + 16), "n"(ALO + 24),
+        "r"(nr) : "memory");
+#undef HG_MMA36_RUN
+}
 // low word of a K-major SWIZZLE_128B descriptor (start address >> 4, LBO field 1)
 __device__ __forceinline__ uint32_t sdesc_sw128_lo(uint32_t saddr) {
     return ((saddr >> 4) & 0x3FFFu) | (1u << 16);
