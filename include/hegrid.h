@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define HEGRID_ABI_VERSION 1
+#define HEGRID_ABI_VERSION 2
 
 typedef enum hegrid_status {
     HEGRID_OK = 0,
@@ -71,11 +71,22 @@ typedef struct hegrid_map {
     double cdelt_lon, cdelt_lat;    /* deg per cell */
 } hegrid_map;
 
-/* Gaussian convolution kernel (readings R1-R3): sigma = fwhm / (2 sqrt(2 ln 2)),
- * support radius R = support_sigma * sigma (the paper's R). */
+/* Convolution kernel w(d) of the great-circle distance d (readings R1-R3; SPEC.md:117-126
+ * KernelSpec{kind, sigma, radius}): sigma = fwhm / (2 sqrt(2 ln 2)), support radius
+ * R = support_sigma * sigma (the paper's R).
+ *   HEGRID_KERNEL_GAUSSIAN (0): w = exp(-d^2 / (2 sigma^2)) for d <= R, else 0;
+ *   HEGRID_KERNEL_TOPHAT   (1): w = 1 for d <= R, else 0 (sigma only sets R).
+ * Zero-initialised structs select the Gaussian.  Other kinds: HEGRID_EINVAL. */
+typedef enum hegrid_kernel_kind {
+    HEGRID_KERNEL_GAUSSIAN = 0,
+    HEGRID_KERNEL_TOPHAT = 1
+} hegrid_kernel_kind;
+
 typedef struct hegrid_kernel {
     double fwhm_deg;        /* > 0 */
     double support_sigma;   /* > 0; 3 is the usual choice */
+    int32_t kind;           /* hegrid_kernel_kind */
+    int32_t reserved;       /* must be 0 */
 } hegrid_kernel;
 
 typedef enum hegrid_engine {

@@ -50,8 +50,10 @@ def _load():
         P = ctypes.c_void_p
         lib.ora_grid_cells.argtypes = [P, P, ctypes.c_int64, P, ctypes.c_int64, P, ctypes.c_int64,
                                        ctypes.POINTER(OraMap), ctypes.c_double, ctypes.c_double,
-                                       P, ctypes.c_int64, P, P, P, ctypes.c_int]
+                                       P, ctypes.c_int64, P, P, P, ctypes.c_int, ctypes.c_int]
         lib.ora_grid_cells.restype = ctypes.c_int
+        lib.ora_weight_tophat.argtypes = [ctypes.c_double] * 2
+        lib.ora_weight_tophat.restype = ctypes.c_double
         lib.ora_neighbours.argtypes = [P, P, ctypes.c_int64, ctypes.POINTER(OraMap),
                                        ctypes.c_double, ctypes.c_double, P, ctypes.c_int64,
                                        P, P, ctypes.c_int]
@@ -113,8 +115,10 @@ def cell_centre(m, i, j):
     return lon.value, lat.value
 
 
-def grid(lon, lat, vals, m, fwhm_deg, support=3.0, channels=None, cells=None, nthreads=0):
-    """Eq. 1 for the given channels (rows of ``vals`` [C][N]) and cells.
+def grid(lon, lat, vals, m, fwhm_deg, support=3.0, channels=None, cells=None, nthreads=0,
+         kernel="gaussian"):
+    """Eq. 1 for the given channels (rows of ``vals`` [C][N]) and cells; ``kernel`` is
+    "gaussian" (Eq. 1's kernel) or "tophat" (1 inside the support).
 
     Returns (out [n_ch][n_cells] fp64 with NaN blanks, W [n_cells], nbr_count [n_cells]).
     ``cells`` = linear indices j*nx+i (None = all, in map order).
@@ -146,7 +150,8 @@ def grid(lon, lat, vals, m, fwhm_deg, support=3.0, channels=None, cells=None, nt
     cnt = np.empty(n_cells, np.int64)
     rc = _load().ora_grid_cells(_p(lon), _p(lat), n, _p(vals), ld, _p(ch), n_ch,
                                 ctypes.byref(mm), float(fwhm_deg), float(support),
-                                _p(cidx), n_cells, _p(out), _p(W), _p(cnt), int(nthreads))
+                                _p(cidx), n_cells, _p(out), _p(W), _p(cnt), int(nthreads),
+                                {"gaussian": 0, "tophat": 1}[kernel])
     if rc != 0:
         raise ValueError(f"oracle rejected arguments (code {rc})")
     return out, W, cnt

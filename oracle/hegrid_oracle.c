@@ -91,17 +91,22 @@ double ora_weight(double d, double sigma, double R) {
     return exp(-(d * d) / (2.0 * sigma * sigma));
 }
 
+/* Tophat kernel (KernelSpec kind "tophat": 1 for d <= R, else 0). */
+double ora_weight_tophat(double d, double R) {
+    return (d <= R) ? 1.0 : 0.0;
+}
+
 /* Neighbour list of one cell: every sample n (ascending) with d <= R.
  * Returns the count; writes idx/w if non-NULL. */
 static int64_t cell_neighbours(const double* lon, const double* lat, int64_t n,
-                               double lon_c, double lat_c, double sigma, double R,
+                               double lon_c, double lat_c, double sigma, double R, int kind,
                                int64_t* idx, double* w) {
     int64_t k = 0;
     for (int64_t s = 0; s < n; ++s) {
         double d = ora_distance_rad(lon_c, lat_c, lon[s], lat[s]);
         if (d <= R) {
             if (idx) idx[k] = s;
-            if (w) w[k] = ora_weight(d, sigma, R);
+            if (w) w[k] = kind == 1 ? ora_weight_tophat(d, R) : ora_weight(d, sigma, R);
             ++k;
         }
     }
@@ -124,14 +129,16 @@ static int valid_inputs(const ora_map* m, double fwhm, double support, int64_t n
  *   wsum       [n_cells] W; may be NULL
  *   nbr_count  [n_cells] number of samples with d <= R; may be NULL
  *   nthreads   OpenMP threads (<= 0: runtime default)
+ *   kind       0 = Gaussian (Eq. 1's kernel, readings R1-R3), 1 = tophat
  * Returns 0 on success, 1 on invalid arguments, 3 on allocation failure.
  */
 int ora_grid_cells(const double* lon, const double* lat, int64_t n,
                    const float* vals, int64_t ld, const int64_t* ch_idx, int64_t n_ch,
                    const ora_map* m, double fwhm_deg, double support,
                    const int64_t* cell_idx, int64_t n_cells,
-                   double* out, double* wsum, int64_t* nbr_count, int nthreads) {
+                   double* out, double* wsum, int64_t* nbr_count, int nthreads, int kind) {
     if (!valid_inputs(m, fwhm_deg, support, n)) return 1;
+    if (kind != 0 && kind != 1) return 1;
     if (n_ch < 0 || (n_ch > 0 && !vals) || (n > 0 && (!lon || !lat))) return 1;
     int64_t ncell_all = (int64_t)m->nx * (int64_t)m->ny;
     if (!cell_idx) n_cells = ncell_all;
@@ -158,7 +165,7 @@ int ora_grid_cells(const double* lon, const double* lat, int64_t n,
             int64_t i = cell % m->nx, j = cell / m->nx;
             double lon_c, lat_c;
             ora_cell_centre(m, i, j, &lon_c, &lat_c);
-            int64_t k = cell_neighbours(lon, lat, n, lon_c, lat_c, sigma, R, idx, w);
+            int64_t k = cell_neighbours(lon, lat, n, lon_c, lat_c, sigma, R, kind, idx, w);
             double W = 0.0;
             for (int64_t t = 0; t < k; ++t) W += w[t];
             if (wsum) wsum[q] = W;
@@ -202,7 +209,7 @@ int ora_neighbours(const double* lon, const double* lat, int64_t n, const ora_ma
         int64_t cell = cell_idx ? cell_idx[q] : q;
         double lon_c, lat_c;
         ora_cell_centre(m, cell % m->nx, cell / m->nx, &lon_c, &lat_c);
-        offsets[q + 1] = cell_neighbours(lon, lat, n, lon_c, lat_c, sigma, R, NULL, NULL);
+        offsets[q + 1] = cell_neighbours(lon, lat, n, lon_c, lat_c, sigma, R, 0, NULL, NULL);
     }
     offsets[0] = 0;
     for (int64_t q = 0; q < n_cells; ++q) offsets[q + 1] += offsets[q];
@@ -213,7 +220,7 @@ int ora_neighbours(const double* lon, const double* lat, int64_t n, const ora_ma
         int64_t cell = cell_idx ? cell_idx[q] : q;
         double lon_c, lat_c;
         ora_cell_centre(m, cell % m->nx, cell / m->nx, &lon_c, &lat_c);
-        cell_neighbours(lon, lat, n, lon_c, lat_c, sigma, R, idx + offsets[q], NULL);
+        cell_neighbours(lon, lat, n, lon_c, lat_c, sigma, R, 0, idx + offsets[q], NULL);
     }
     return 0;
 }

@@ -10,7 +10,7 @@ import numpy as np
 
 from . import _binding as abi
 from ._binding import (HEGRID_ENGINE_TC, HEGRID_LAYOUT_PLAN_NC, HEGRID_LAYOUT_USER_CN, HegridError,  # noqa: F401
-                       hegrid_abi_version, hegrid_grid, hegrid_grid_device,
+                       KERNELS, hegrid_abi_version, hegrid_grid, hegrid_grid_device,
                        hegrid_launch_count, hegrid_neighbours, hegrid_permute_device,
                        hegrid_plan_create, hegrid_plan_create_device, hegrid_plan_destroy,
                        hegrid_plan_info, hegrid_plan_permutation, hegrid_profile_enable,
@@ -41,7 +41,7 @@ class Plan:
     ENGINES = {"auto": 0, "simt": 1, "tc": 2}
 
     def __init__(self, lon, lat, map, fwhm_deg, support_sigma=3.0, device=0, n_streams=0,
-                 channel_block=0, stream=None, engine="auto"):
+                 channel_block=0, stream=None, engine="auto", kernel="gaussian"):
         self.map = dict(map) if isinstance(map, dict) else map
         self.nx, self.ny = int(self.map["nx"]), int(self.map["ny"])
         self.device = device
@@ -52,12 +52,14 @@ class Plan:
             lat = lat.to(torch.float64).contiguous()
             self.n = lon.shape[0]
             self._h = hegrid_plan_create_device(lon, lat, self.n, self.map, fwhm_deg,
-                                                support_sigma, opts, _stream_handle(stream))
+                                                support_sigma, opts, _stream_handle(stream),
+                                                KERNELS[kernel])
         else:
             lon = np.ascontiguousarray(np.asarray(lon), np.float64)
             lat = np.ascontiguousarray(np.asarray(lat), np.float64)
             self.n = lon.shape[0]
-            self._h = hegrid_plan_create(lon, lat, self.map, fwhm_deg, support_sigma, opts)
+            self._h = hegrid_plan_create(lon, lat, self.map, fwhm_deg, support_sigma, opts,
+                                         KERNELS[kernel])
 
     # -------------------------------------------------------------- lifetime
     def close(self):

@@ -38,7 +38,12 @@ class hegrid_map(ctypes.Structure):
 
 
 class hegrid_kernel(ctypes.Structure):
-    _fields_ = [("fwhm_deg", ctypes.c_double), ("support_sigma", ctypes.c_double)]
+    _fields_ = [("fwhm_deg", ctypes.c_double), ("support_sigma", ctypes.c_double),
+                ("kind", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+HEGRID_KERNEL_GAUSSIAN, HEGRID_KERNEL_TOPHAT = 0, 1
+KERNELS = {"gaussian": HEGRID_KERNEL_GAUSSIAN, "tophat": HEGRID_KERNEL_TOPHAT}
 
 
 class hegrid_opts(ctypes.Structure):
@@ -144,12 +149,13 @@ def make_opts(device=0, n_streams=0, channel_block=0, engine=0) -> hegrid_opts:
 
 # ----------------------------------------------------------------- C-ABI names
 def hegrid_plan_create(lon_deg: np.ndarray, lat_deg: np.ndarray, m, fwhm_deg: float,
-                       support_sigma: float = 3.0, opts: hegrid_opts | None = None) -> int:
+                       support_sigma: float = 3.0, opts: hegrid_opts | None = None,
+                       kind: int = HEGRID_KERNEL_GAUSSIAN) -> int:
     lon = np.ascontiguousarray(lon_deg, np.float64)
     lat = np.ascontiguousarray(lat_deg, np.float64)
     if lon.shape != lat.shape or lon.ndim != 1:
         raise ValueError("lon/lat must be equal-length 1-D arrays")
-    mm, kk = make_map(m), hegrid_kernel(fwhm_deg, support_sigma)
+    mm, kk = make_map(m), hegrid_kernel(fwhm_deg, support_sigma, kind, 0)
     out = PLAN()
     _check(load().hegrid_plan_create(_ptr(lon), _ptr(lat), lon.shape[0], ctypes.byref(mm),
                                      ctypes.byref(kk), ctypes.byref(opts) if opts else None,
@@ -159,8 +165,8 @@ def hegrid_plan_create(lon_deg: np.ndarray, lat_deg: np.ndarray, m, fwhm_deg: fl
 
 def hegrid_plan_create_device(d_lon, d_lat, n: int, m, fwhm_deg: float,
                               support_sigma: float = 3.0, opts: hegrid_opts | None = None,
-                              stream: int = 0) -> int:
-    mm, kk = make_map(m), hegrid_kernel(fwhm_deg, support_sigma)
+                              stream: int = 0, kind: int = HEGRID_KERNEL_GAUSSIAN) -> int:
+    mm, kk = make_map(m), hegrid_kernel(fwhm_deg, support_sigma, kind, 0)
     out = PLAN()
     _check(load().hegrid_plan_create_device(_ptr(d_lon), _ptr(d_lat), n, ctypes.byref(mm),
                                             ctypes.byref(kk),

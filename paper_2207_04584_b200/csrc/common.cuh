@@ -38,6 +38,9 @@ struct Geom {
     // tensor-core engine's weight patches; t >= t_in: inside, t < t_out: outside, else the
     // guard band (t_in = neg_k2 R2_lo, t_out = neg_k2 R2_hi; neg_k2 < 0 flips the order)
     float tK0, tK1, tK2, t_in, t_out;
+    // kernel shape: w = 2^(wexp * t): wexp = 1 for the Gaussian, 0 for the tophat (w = 1
+    // inside the support; the support test keeps using the Gaussian-scaled t)
+    float wexp;
 };
 
 // Per-sample plan data in plan order.

@@ -296,6 +296,7 @@ static hegrid_status make_geom(hegrid_plan_s* p, std::vector<int>& mrow,
     g.tK2 = (float)(32.0 / 45.0 * nk2);
     g.t_in = (float)(nk2 * R2 * (1.0 - 1e-5));
     g.t_out = (float)(nk2 * R2 * (1.0 + 1e-5));
+    g.wexp = p->kern.kind == HEGRID_KERNEL_TOPHAT ? 0.0f : 1.0f;
     return HEGRID_OK;
 }
 

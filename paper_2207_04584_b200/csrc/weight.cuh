@@ -85,7 +85,7 @@ __device__ __forceinline__ float pair_weight(const Geom& g, const PlanDev& pd, i
         double2 ll = pd.ll[p];
         in = support_fp64(g, i, j, ll.x, ll.y);
     }
-    return in ? ex2_approx(d2 * g.neg_k2) : 0.0f;
+    return in ? ex2_approx(d2 * g.neg_k2 * g.wexp) : 0.0f;
 }
 
 // Weights of a 4 x NCOL (sample x cell) patch: samples s[0..3] (plan positions p0..p0+3)
@@ -124,7 +124,7 @@ __device__ __forceinline__ void patch_weights(const Geom& g, const PlanDev& pd, 
             const float h = fmaf(ccs, sbv, sa);
             const float t = h * fmaf(h, fmaf(h, g.tK2, g.tK1), g.tK0);
             band |= (t < g.t_in) & (t >= g.t_out);
-            w[u][j] = t >= g.t_out ? ex2_approx(t) : 0.0f;     // band pairs provisionally in
+            w[u][j] = t >= g.t_out ? ex2_approx(t * g.wexp) : 0.0f;   // band pairs provisionally in
         }
     }
     if (band) {   // rare: find the guard-band pairs again and decide them in fp64

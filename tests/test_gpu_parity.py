@@ -327,3 +327,20 @@ def test_tc_pw_and_otf_bit_identical(monkeypatch):
     with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, engine="tc", channel_block=512) as p:
         out_h, W_h = p.grid(vals.numpy())
     np.testing.assert_array_equal(np.asarray(out_h).reshape(res[0][0].shape), res[0][0])
+
+
+@pytest.mark.parametrize("engine", ["simt", "tc_otf", "tc_pw"])
+def test_tophat_kernel_parity(engine, monkeypatch):
+    """SPEC.md:117-126 tophat kernel through the C-ABI (hegrid_kernel.kind = TOPHAT): W is
+    the exact neighbour count, the map the neighbour mean, against the oracle."""
+    engine = engine_env(engine, monkeypatch)
+    w = small_workload("cfg2", n=120 * 100, tracks=120, per_track=100, nx=40, ny=37,
+                       field_lon=0.7, field_lat=0.6, channels=520)
+    lon, lat, vals = make_inputs(w)
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, engine=engine, kernel="tophat") as p:
+        out, W = p.grid(vals.cuda())
+        out, W = out.cpu().numpy(), W.cpu().numpy()
+    o, Wo, cnt = oracle.grid(lon.numpy(), lat.numpy(), vals.numpy(), w.map, w.fwhm_deg,
+                             w.support, kernel="tophat")
+    np.testing.assert_array_equal(W.reshape(-1).astype(np.int64), cnt)
+    compare(out.reshape(520, -1), W.reshape(-1), o, Wo)

@@ -330,3 +330,35 @@ def test_thread_count_does_not_change_results():
     b = oracle.grid(lon, lat, v, m, 3.0 / 60, nthreads=4)
     for x, y in zip(a, b):
         np.testing.assert_array_equal(x, y)
+
+
+def test_tophat_kernel_is_plain_neighbour_mean():
+    """SPEC.md:117-126 tophat kernel (1 for d <= R, else 0): W is the neighbour count and the
+    map is the plain mean of the values within R.  Neighbour sets from sklearn's BallTree
+    (haversine) and the mean from numpy: nothing shared with the oracle's loop."""
+    from sklearn.neighbors import BallTree
+    rng = np.random.default_rng(33)
+    N = 6000
+    lon = 30 + rng.uniform(-0.2, 0.2, N)
+    lat = 41 + rng.uniform(-0.2, 0.2, N)
+    v = rng.normal(10, 2, (2, N)).astype(np.float32)
+    m = mk_map(16, 14, 30.0, 41.0, 1.0 / 60)
+    fwhm = 3.0 / 60
+    out, W, cnt = oracle.grid(lon, lat, v, m, fwhm, kernel="tophat")
+    R = 3.0 * math.radians(fwhm / FWHM2SIG)
+    tree = BallTree(np.radians(np.stack([lat, lon], 1)), metric="haversine")
+    jj, ii = np.divmod(np.arange(16 * 14), 16)
+    cl = 30 + (ii + 1 - 8.5) / 60
+    cb = 41 + (jj + 1 - 7.5) / 60
+    res = tree.query_radius(np.radians(np.stack([cb, cl], 1)), r=R)
+    for q in range(16 * 14):
+        s = res[q]
+        assert W[q] == len(s) == cnt[q]
+        if len(s):
+            np.testing.assert_allclose(out[:, q], v[:, s].astype(np.float64).mean(1), rtol=1e-12)
+        else:
+            assert np.all(np.isnan(out[:, q]))
+    # the Gaussian and the tophat share the support: identical neighbour counts and blanks
+    og, Wg, cg = oracle.grid(lon, lat, v, m, fwhm)
+    np.testing.assert_array_equal(cg, cnt)
+    assert np.all((Wg > 0) == (W > 0))
