@@ -344,3 +344,24 @@ def test_tophat_kernel_parity(engine, monkeypatch):
                              w.support, kernel="tophat")
     np.testing.assert_array_equal(W.reshape(-1).astype(np.int64), cnt)
     compare(out.reshape(520, -1), W.reshape(-1), o, Wo)
+
+
+@pytest.mark.parametrize("engine", ["simt", "tc"])
+def test_cell_sharded_plans_assemble_to_full_map(engine, monkeypatch):
+    """NEXT-3 cell sharding on the GPU path: three map-row blocks, each gridded by its own
+    sub-map plan (as three ranks would), assemble to the full map within the parity rule."""
+    from paper_2207_04584_b200.shard import row_shard, sub_map
+    engine = engine_env(engine, monkeypatch)
+    w = small_workload("cfg3", n=60_000, field_lon=0.3, field_lat=0.3, nx=20, ny=19, channels=5)
+    lon, lat, vals = make_inputs(w)
+    out = np.empty((5, w.ny, w.nx), np.float32)
+    W = np.empty((w.ny, w.nx), np.float32)
+    for r in range(3):
+        j0, j1 = row_shard(w.ny, 3, r)
+        sm = sub_map(w.map, j0, j1)
+        with Plan(lon.numpy(), lat.numpy(), sm, w.fwhm_deg, engine=engine) as p:
+            o, ww = p.grid(vals.numpy())
+        out[:, j0:j1] = np.asarray(o).reshape(5, j1 - j0, w.nx)
+        W[j0:j1] = np.asarray(ww).reshape(j1 - j0, w.nx)
+    o, Wo, _ = oracle_grid(w, lon, lat, vals)
+    compare(out.reshape(5, -1), W.reshape(-1), o, Wo)

@@ -12,7 +12,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2207_04584_b200.shard import channel_shard, grid_sharded
+from paper_2207_04584_b200.shard import channel_shard, grid_cell_sharded, grid_sharded, row_shard, sub_map
 
 
 def _worker(rank, world, port, path, C, N, out_shape):
@@ -64,3 +64,61 @@ def test_channel_sharded_grid_equals_single_process(world):
         a, b = channel_shard(C, world, r)
         cover[a:b] += 1
     assert np.all(cover == 1)
+
+
+def _cell_worker(rank, world, port, path, C, N, out_shape):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import synth
+    w = synth.CONFIGS["cfg3"].with_(n=N, channels=C, nx=13, ny=11, field_lon=0.3, field_lat=0.3)
+    lon, lat = synth.coords(w)
+    vals = synth.values(w, lon, lat).numpy()
+    out = np.memmap(path, dtype=np.float64, mode="r+", shape=out_shape)
+
+    def grid_fn(sm):
+        o, _, _ = oracle.grid(lon.numpy(), lat.numpy(), vals, sm, w.fwhm_deg, w.support, nthreads=1)
+        return o.reshape(C, sm["ny"], sm["nx"])
+
+    grid_cell_sharded(grid_fn, w.map, world, rank, out)
+    out.flush()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_cell_sharded_grid_equals_single_process(world):
+    """NEXT-3: ranks own map-row blocks (sub-map plans), the assembled map equals the
+    single-process map bit for bit (same cell centres, same per-cell sums)."""
+    import oracle
+    import synth
+    C, N = 3, 3000
+    w = synth.CONFIGS["cfg3"].with_(n=N, channels=C, nx=13, ny=11, field_lon=0.3, field_lat=0.3)
+    shape = (C, w.ny, w.nx)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "out.bin")
+        np.memmap(path, dtype=np.float64, mode="w+", shape=shape).flush()
+        port = 31500 + (os.getpid() % 2000)
+        mp.spawn(_cell_worker, args=(world, port, path, C, N, shape), nprocs=world, join=True)
+        got = np.array(np.memmap(path, dtype=np.float64, mode="r", shape=shape))
+    lon, lat = synth.coords(w)
+    vals = synth.values(w, lon, lat).numpy()
+    ref, _, _ = oracle.grid(lon.numpy(), lat.numpy(), vals, w.map, w.fwhm_deg, w.support)
+    ref = ref.reshape(shape)
+    np.testing.assert_array_equal(np.isnan(got), np.isnan(ref))
+    np.testing.assert_array_equal(got[~np.isnan(ref)], ref[~np.isnan(ref)])
+
+
+def test_row_shard_covers_rows_once():
+    for ny in (1, 7, 300, 512):
+        for world in (1, 2, 3, 8):
+            rows = [r for k in range(world) for r in range(*row_shard(ny, world, k))]
+            assert rows == list(range(ny))
+    m = {"nx": 5, "ny": 9, "crval_lon": 30.0, "crval_lat": 41.0, "crpix_x": 3.0,
+         "crpix_y": 5.0, "cdelt_lon": 0.1, "cdelt_lat": 0.1}
+    s = sub_map(m, 4, 9)
+    for jp in range(5):
+        lat_sub = s["crval_lat"] + (jp + 1 - s["crpix_y"]) * s["cdelt_lat"]
+        lat_full = m["crval_lat"] + (jp + 4 + 1 - m["crpix_y"]) * m["cdelt_lat"]
+        assert lat_sub == lat_full
