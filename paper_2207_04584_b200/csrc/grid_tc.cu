@@ -539,7 +539,8 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
            PlanDev pd, const uint4* __restrict__ sched,
            const uint32_t* __restrict__ tile_off, const float* __restrict__ wsum,
            const uint8_t* __restrict__ wimg, const uint32_t* __restrict__ wslot,
-           int C, int tiles, int cgroup, int super_, int snake, float* __restrict__ out,
+           int C, int tiles, int cgroup, int super_, int snake, int nsplit,
+           float* __restrict__ part, float* __restrict__ out,
            float* __restrict__ wout, int dbg_in) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_raw);
@@ -573,7 +574,9 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     int tile, cblk;
     {
         const int ncb = (C + TC_M - 1) / TC_M;
-        const int lin = blockIdx.x, grp = lin / (tiles * cgroup), within = lin % (tiles * cgroup);
+        // few CTAs (few tiles x channel blocks): each tile's entries are split into nsplit
+        // contiguous parts run by different CTAs, whose partial sums k_tc_reduce adds up
+        const int lin = blockIdx.x / nsplit, grp = lin / (tiles * cgroup), within = lin % (tiles * cgroup);
         const int gsz = min(cgroup, ncb - grp * cgroup);
         const int L = within / gsz;
         cblk = grp * cgroup + within % gsz;
@@ -587,8 +590,11 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     }
     const int i0 = (tile % tiles_x) * TC_TW, j0 = (tile / tiles_x) * TC_TH;
     const int cb = cblk * TC_M;
-    const uint4* cs = sched + tile_off[tile];
-    const int nchunks = (int)(tile_off[tile + 1] - tile_off[tile]);
+    const int sp = blockIdx.x % nsplit;              // part of the tile's entries
+    const uint32_t e_all = tile_off[tile + 1] - tile_off[tile];
+    const uint32_t e_begin = (uint32_t)((uint64_t)e_all * sp / nsplit);
+    const uint4* cs = sched + tile_off[tile] + e_begin;
+    const int nchunks = (int)((uint64_t)e_all * (sp + 1) / nsplit - e_begin);
     // Tiles of odd tile rows walk their entries backwards (bottom bin rows first): a tile and
     // the one below it then read the bin rows they share at the same stage of their lifetimes,
     // while both are resident, so the second read hits L2.  The order is fixed per tile.
@@ -853,7 +859,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         // (static indices), so no global-load latency sits on the loop.  (An L2 prefetch of
         // the next group's weights, HG_TC_WPF, measured slower: the CTAs of a tile share them.)
         if (lane == 0) {
-            const uint32_t* ws = wslot + tile_off[tile];
+            const uint32_t* ws = wslot + tile_off[tile] + e_begin;
             constexpr int G = 8;
             uint32_t zc[G], sc[G], zn[G], sn[G], zf[G], sf[G];
             auto ldg = [&](int g0, uint32_t (&z)[G], uint32_t (&sl)[G]) {
@@ -1115,12 +1121,16 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const int ch = cb + row, i = i0 + x, j = j0 + y;
             if (ch < C && i < g.nx && j < g.ny) {
                 const float S = sm.M[row][y * TC_TW + x];
-                const float W = sm.Wt[y * TC_TW + x];
-                out[(int64_t)ch * cells + (int64_t)j * g.nx + i] = W > 0.0f ? __fdiv_rn(S, W) : qnan;
+                if (nsplit > 1) {                      // partial sum of this part
+                    part[((int64_t)sp * C + ch) * cells + (int64_t)j * g.nx + i] = S;
+                } else {
+                    const float W = sm.Wt[y * TC_TW + x];
+                    out[(int64_t)ch * cells + (int64_t)j * g.nx + i] = W > 0.0f ? __fdiv_rn(S, W) : qnan;
+                }
             }
         }
     }
-    if (cblk == 0 && wout != nullptr && tid < TC_TW * TC_TH) {
+    if (cblk == 0 && sp == 0 && wout != nullptr && tid < TC_TW * TC_TH) {
         const int i = i0 + tid % TC_TW, j = j0 + tid / TC_TW;
         if (i < g.nx && j < g.ny) wout[(int64_t)j * g.nx + i] = __ldg(&wsum[(int64_t)j * g.nx + i]);
     }
@@ -1149,6 +1159,19 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc(tmem, TMEM_COLS);
+}
+
+// Split tiles: out = (sum of the parts' partial sums, in part order) / W, NaN where W = 0.
+__global__ void k_tc_reduce(const float* __restrict__ part, int nsplit, int64_t n, int64_t cells,
+                            const float* __restrict__ wsum, float* __restrict__ out) {
+    const float qnan = __int_as_float(0x7fc00000);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const float W = __ldg(&wsum[e % cells]);
+        float S = 0.0f;
+        for (int k = 0; k < nsplit; ++k) S += __ldg(&part[k * n + e]);
+        out[e] = W > 0.0f ? __fdiv_rn(S, W) : qnan;
+    }
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
@@ -1189,7 +1212,20 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     int C = (int)n_channels;
     int tiles = ((g.nx + TC_TW - 1) / TC_TW) * ((g.ny + TC_TH - 1) / TC_TH);
     const int ncb = (C + TC_M - 1) / TC_M;
-    dim3 grid(tiles * ncb);
+    // split the tiles' entry lists when the grid would leave SMs idle: about four waves
+    int nsplit = 1;
+    {
+        int nsm = 148;
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t ctas = (int64_t)tiles * ncb;
+        if (ctas < 2 * nsm) nsplit = (int)std::min<int64_t>(8, std::max<int64_t>(1, (4 * nsm + ctas / 2) / ctas));
+        if (const char* e = getenv("HEGRID_TC_SPLIT")) nsplit = std::max(1, std::min(16, atoi(e)));
+    }
+    dim3 grid(tiles * ncb * nsplit);
+    float* d_part = nullptr;
+    if (nsplit > 1)
+        HG_TRY(cudaMallocAsync(&d_part, (size_t)nsplit * C * (size_t)g.nx * g.ny * sizeof(float), st));
     size_t smem = sizeof(TcSmem);
     int dbg = 0;
     if (const char* e = getenv("HEGRID_TC_DEBUG")) dbg = atoi(e);
@@ -1213,8 +1249,15 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     HG_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched, p->d_tc_tile_off,
                                          p->d_tc_wsum, p->d_tc_wimg, p->d_tc_wslot, C, tiles, cgroup,
-                                         super_, snake, d_out, d_weight, dbg);
+                                         super_, snake, nsplit, d_part, d_out, d_weight, dbg);
     count_launch();
+    if (nsplit > 1) {
+        const int64_t n = (int64_t)C * g.nx * g.ny;
+        k_tc_reduce<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(
+            d_part, nsplit, n, (int64_t)g.nx * g.ny, p->d_tc_wsum, d_out);
+        count_launch();
+        cudaFreeAsync(d_part, st);
+    }
     if (dbg & 32) {
         unsigned long long h[16];
         cudaStreamSynchronize(st);
