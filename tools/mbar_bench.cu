@@ -45,8 +45,25 @@ __global__ void k(unsigned long long* out, int iters) {
         }
         tc::wait_st();
         long long t5 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            tc::fence_before_sync();
+            __syncwarp();
+            tc::fence_after_sync();
+        }
+        long long t6 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            tc::tmem_st16(tb + (i & 3) * 16, r);
+            tc::wait_st();
+            tc::fence_before_sync();
+            __syncwarp();
+            if (threadIdx.x == 0) tc::mbar_arrive(&bar[1]);
+            tc::mbar_wait(&bar[1], i & 1);
+            tc::fence_after_sync();
+        }
+        long long t7 = clock64();
         if (threadIdx.x == 0 && blockIdx.x == 0) {
             out[0] = t1 - t0; out[1] = t2 - t1; out[2] = t3 - t2; out[3] = t4 - t3; out[4] = t5 - t4;
+            out[5] = t6 - t5; out[6] = t7 - t6;
         }
     }
     __syncthreads();
@@ -54,17 +71,19 @@ __global__ void k(unsigned long long* out, int iters) {
 }
 int main() {
     unsigned long long* d;
-    cudaMalloc(&d, 64);
+    cudaMalloc(&d, 128);
     const int iters = 1000;
     k<<<1, 128>>>(d, iters);
     cudaError_t e = cudaDeviceSynchronize();
-    unsigned long long h[5];
-    cudaMemcpy(h, d, 40, cudaMemcpyDeviceToHost);
+    unsigned long long h[7];
+    cudaMemcpy(h, d, 56, cudaMemcpyDeviceToHost);
     printf("%s\n", cudaGetErrorString(e));
     printf("try_wait (done phase, suspend hint): %.1f cyc\n", h[0] / (double)iters);
     printf("test_wait spin (done phase):         %.1f cyc\n", h[1] / (double)iters);
     printf("arrive + wait (own phase):           %.1f cyc\n", h[2] / (double)iters);
     printf("tcgen05.st x16 + wait::st:           %.1f cyc\n", h[3] / (double)iters);
     printf("2 x tcgen05.st x16 (pipelined):      %.1f cyc\n", h[4] / (double)iters);
+    printf("tcgen05.fence before/after + syncwarp: %.1f cyc\n", h[5] / (double)iters);
+    printf("st + wait + fence + arrive + wait + fence: %.1f cyc\n", h[6] / (double)iters);
     return 0;
 }
