@@ -98,9 +98,11 @@ static hegrid_status create_common(const double* d_lon, const double* d_lat, int
 hegrid_status launch_accumulate(const hegrid_plan_s* p, const float* d_v, int64_t ldv,
                                 int64_t n_channels, float* d_out, float* d_weight,
                                 cudaStream_t st) {
-    if (p->opts.engine == HEGRID_ENGINE_TC)
-        return launch_accumulate_tc(p, d_v, ldv, n_channels, d_out, d_weight, st);
-    return launch_accumulate_simt(p, d_v, ldv, n_channels, d_out, d_weight, st);
+    // AUTO takes the tensor-core engine: faster on every measured configuration (DESIGN.md
+    // section 11: cfg2 1.5 vs 4.4 ms, cfg3 7.3 vs 109 ms, cfg4 14 vs 68 ms)
+    if (p->opts.engine == HEGRID_ENGINE_SIMT)
+        return launch_accumulate_simt(p, d_v, ldv, n_channels, d_out, d_weight, st);
+    return launch_accumulate_tc(p, d_v, ldv, n_channels, d_out, d_weight, st);
 }
 
 }  // namespace hg
