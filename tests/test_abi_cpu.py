@@ -67,6 +67,9 @@ def test_argument_validation_without_gpu():
     with pytest.raises(b.HegridError) as e:
         b.hegrid_plan_create(lon, lat, m, 0.05, support_sigma=0.0)
     assert e.value.code == 1
+    with pytest.raises(b.HegridError) as e:          # unknown kernel kind
+        b.hegrid_plan_create(lon, lat, m, 0.05, kind=7)
+    assert e.value.code == 1
     # NULL plan
     assert b.load().hegrid_grid(None, None, 0, None, None) == 1
     assert b.load().hegrid_plan_info(None, None) == 1
