@@ -710,7 +710,13 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const int sb = PW ? c % NBF : c % NBS;
             {
                 TPROF_BEGIN;
+#ifdef HG_TC_NAMED_AFULL
+                // named barrier 1 + sa: the A warps arrive, the issuers sync (≈ 20 cycles per
+                // hand-off against ≈ 90 through an mbarrier, tools/handoff_bench.cu)
+                asm volatile("bar.sync %0, %1;" :: "r"(1 + sa), "r"(32 * (A_WARPS + NI)) : "memory");
+#else
                 HG_WAIT_CRIT(&sm.a_full[sa], (c / NA) & 1);
+#endif
                 TPROF_END(0);
             }
             if (issuer == 0 && lane == 0) TL(3, c);
@@ -1018,8 +1024,12 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             tc::wait_st();
             if (warp == 4 && lane == 0) TL(9, c);
             tc::fence_before_sync();
+#ifdef HG_TC_NAMED_AFULL
+            asm volatile("bar.arrive %0, %1;" :: "r"(1 + c % NA), "r"(32 * (A_WARPS + NI)) : "memory");
+#else
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&sm.a_full[c % NA]);
+#endif
             if (warp == 4 && lane == 0) TL(2, c);
             if (c + 1 < nchunks) {
                 const int cn = c + 1;
