@@ -103,8 +103,10 @@ constexpr int SEG_DENSE = HG_TC_SEG, SEG_SPARSE = HG_TC_SEG_SPARSE;
 // A block touched by at most this many chunks in the whole tile accumulates few enough MMAs
 // per segment at SEG_SPARSE (measured: max rel err 4e-6 at cfg4, where the max is 70)
 constexpr uint32_t TC_CPB_SPARSE = 80 / KA;
-// PW mode (precomputed weight image) from this many 128-channel blocks per launch
-constexpr unsigned TC_PW_MIN_CBLOCKS = 4;
+// PW mode (precomputed weight image) from this many 128-channel blocks per launch: measured
+// faster than on-the-fly weights even for one block (cfg3 4.7 vs 7.2 ms, cfg2 1.0 vs 1.5 ms),
+// so whenever the image fits the memory budget
+constexpr unsigned TC_PW_MIN_CBLOCKS = 1;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t D_COLS = TC_NB * TC_N;      // one accumulator buffer: 12 blocks x 16 columns
 #ifndef HG_TC_ND
@@ -1241,8 +1243,8 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     if (const char* e = getenv("HEGRID_TC_DEBUG")) dbg = atoi(e);
     const bool sparse = p->tc_max_cpb <= TC_CPB_SPARSE;
     const int SEG = sparse ? SEG_SPARSE : SEG_DENSE;
-    // Precomputed weights pay once several channel blocks share them (each block would
-    // otherwise recompute every weight); HEGRID_TC_PW=0/1 forces the choice.
+    // Precomputed weights (read once per channel block) beat recomputing them in the kernel
+    // even for a single block; HEGRID_TC_PW=0/1 forces the choice.
     int want_pw = ncb >= (int)TC_PW_MIN_CBLOCKS;
     if (const char* e = getenv("HEGRID_TC_PW")) want_pw = atoi(e);
     const bool pw = want_pw && ensure_tc_wimage(p, st);
