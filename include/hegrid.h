@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define HEGRID_ABI_VERSION 2
+#define HEGRID_ABI_VERSION 3
 
 typedef enum hegrid_status {
     HEGRID_OK = 0,
@@ -102,6 +102,13 @@ typedef struct hegrid_opts {
     int32_t channel_block;  /* channels per pipeline block in hegrid_grid (0 = auto; rounded
                                up to a multiple of 4) */
     int32_t engine;         /* hegrid_engine */
+    int64_t weight_image_max_bytes;  /* tensor-core engine: cap on the plan's precomputed weight
+                               image (every (cell, sample) weight of the chunk schedule, built
+                               once per plan on first use and kept for the plan's lifetime;
+                               DESIGN.md sec. 6).  0 = auto (at most 1/4 of the device memory
+                               free at build time), > 0 = at most this many bytes, < 0 = never
+                               (weights computed in every launch).  A plan whose image did not
+                               fit retries on later calls. */
 } hegrid_opts;
 
 /* Value layouts accepted by hegrid_grid_device / hegrid_permute_device. */
@@ -127,6 +134,7 @@ typedef struct hegrid_plan_stats {
     int32_t nrow, ncol;         /* bin grid (cells + margins) */
     int32_t mlat, mlon;         /* margins in bins */
     double sigma_deg, radius_deg;
+    int64_t weight_image_bytes; /* device bytes of the precomputed weight image (0 = none) */
 } hegrid_plan_stats;
 
 /* ---- plan: spatial index (PAPER.md:177-192 steps 1,2,4; Algorithm 1 region lookup) ----
@@ -170,7 +178,11 @@ hegrid_status hegrid_grid(hegrid_plan_t plan, const float* data, int64_t n_chann
  * d_data: device, layout per `layout` (hegrid_layout) with row stride ld (elements).
  * d_out: device [C][ny][nx] fp32; d_weight: device [ny][nx] or NULL.
  * Enqueued on `stream` (cudaStream_t); asynchronous.  USER_CN input is permuted through
- * an internal device scratch in channel blocks (extra HBM traffic). */
+ * a device scratch taken from the plan's stream-ordered pool on `stream` (extra HBM
+ * traffic), so calls on different streams never share it.
+ * Non-finite values (NaN, +-Inf; reading R15): the cells within R of such a sample get
+ * the IEEE result of Eq. 1's sum (NaN, or +-Inf), exactly like the fp64 definition; all
+ * other cells are unaffected.  |values| >= 2^128 (1 - 2^-12) count as +-Inf. */
 hegrid_status hegrid_grid_device(hegrid_plan_t plan, const float* d_data, int64_t n_channels,
                                  int64_t ld, int32_t layout, float* d_out, float* d_weight,
                                  void* stream);
@@ -181,10 +193,15 @@ hegrid_status hegrid_grid_device(hegrid_plan_t plan, const float* d_data, int64_
 hegrid_status hegrid_permute_device(hegrid_plan_t plan, const float* d_user, int64_t n_channels,
                                     int64_t ld_user, float* d_plan, int64_t ld_plan, void* stream);
 
-/* Neighbour sets of cells [cell_begin, cell_end) (linear j*nx+i), computed on the device
- * with the same candidate lookup and predicate as the hot path.  offsets: host
+/* Neighbour sets of cells [cell_begin, cell_end) (linear j*nx+i): Algorithm 1's gather set
+ * {n : d(cell, s_n) <= R} (line "if d(target_cell[], raw_data[i]) <= R"),
+ * enumerated on the device from the very pairs the plan's engine accumulates: for the
+ * tensor-core engine (AUTO / TC) its per-tile chunk schedule and its weight expression
+ * (a pair counts iff its weight is > 0), for the SIMT engine its per-cell candidate ranges
+ * and predicate.  A pair the engine misses is missing here too, so comparing this set with
+ * the fp64 definition checks the hot path's gather.  offsets: host
  * [cell_end-cell_begin+1]; sample_idx: host CSR of original sample indices, ascending
- * within each cell; NULL = counts only.  Blocking. */
+ * within each cell; NULL = counts only.  Blocking.  Errors: EINVAL (range), ECUDA, ENOMEM. */
 hegrid_status hegrid_neighbours(hegrid_plan_t plan, int64_t cell_begin, int64_t cell_end,
                                 int64_t* offsets, int64_t* sample_idx);
 
@@ -198,6 +215,16 @@ hegrid_status hegrid_sort_u32(const uint32_t* keys, int64_t n, int32_t* perm, in
  * since the last read, and resets them. */
 hegrid_status hegrid_profile_enable(hegrid_plan_t plan, int32_t enable);
 hegrid_status hegrid_profile_read(hegrid_plan_t plan, double* ms, int64_t* launches);
+
+/* Pipeline trace of the last hegrid_grid call made while profiling was enabled
+ * (hegrid_profile_enable): one row of 5 doubles per channel block,
+ *   {slot (stream index), h2d_start, h2d_end, compute_end, d2h_end},
+ * times in ms from the call's first event, from CUDA events recorded on each slot's stream
+ * around the block's H2D copy, its device permute + accumulate (+ fix-up) and its D2H copy
+ * (the paper's T2 / T3 / T4 stages, overlapped across streams as in
+ * :279-294).  buf: host [cap_rows][5] or NULL (count only); *n_rows = rows available. */
+hegrid_status hegrid_pipeline_trace(hegrid_plan_t plan, double* buf, int64_t cap_rows,
+                                    int64_t* n_rows);
 
 /* Number of kernels this library has launched in this process (all plans). */
 int64_t hegrid_launch_count(void);

@@ -13,7 +13,8 @@ from ._binding import (HEGRID_ENGINE_TC, HEGRID_LAYOUT_PLAN_NC, HEGRID_LAYOUT_US
                        KERNELS, hegrid_abi_version, hegrid_grid, hegrid_grid_device,
                        hegrid_launch_count, hegrid_neighbours, hegrid_permute_device,
                        hegrid_plan_create, hegrid_plan_create_device, hegrid_plan_destroy,
-                       hegrid_plan_info, hegrid_plan_permutation, hegrid_profile_enable,
+                       hegrid_pipeline_trace, hegrid_plan_info, hegrid_plan_permutation,
+                       hegrid_profile_enable,
                        hegrid_profile_read, hegrid_sort_u32, hegrid_status_string, make_map,
                        make_opts)
 from .shard import channel_shard  # noqa: F401
@@ -41,11 +42,13 @@ class Plan:
     ENGINES = {"auto": 0, "simt": 1, "tc": 2}
 
     def __init__(self, lon, lat, map, fwhm_deg, support_sigma=3.0, device=0, n_streams=0,
-                 channel_block=0, stream=None, engine="auto", kernel="gaussian"):
+                 channel_block=0, stream=None, engine="auto", kernel="gaussian",
+                 weight_image_max_bytes=0):
         self.map = dict(map) if isinstance(map, dict) else map
         self.nx, self.ny = int(self.map["nx"]), int(self.map["ny"])
         self.device = device
-        opts = make_opts(device, n_streams, channel_block, self.ENGINES[engine])
+        opts = make_opts(device, n_streams, channel_block, self.ENGINES[engine],
+                         weight_image_max_bytes)
         if hasattr(lon, "is_cuda") and lon.is_cuda:
             import torch
             lon = lon.to(torch.float64).contiguous()
@@ -154,3 +157,7 @@ class Plan:
 
     def profile_read(self):
         return hegrid_profile_read(self._h)
+
+    def pipeline_trace(self):
+        """Per-block stage times of the last profiled host grid call (hegrid_pipeline_trace)."""
+        return hegrid_pipeline_trace(self._h)

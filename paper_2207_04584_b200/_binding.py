@@ -48,7 +48,8 @@ KERNELS = {"gaussian": HEGRID_KERNEL_GAUSSIAN, "tophat": HEGRID_KERNEL_TOPHAT}
 
 class hegrid_opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("n_streams", ctypes.c_int32),
-                ("channel_block", ctypes.c_int32), ("engine", ctypes.c_int32)]
+                ("channel_block", ctypes.c_int32), ("engine", ctypes.c_int32),
+                ("weight_image_max_bytes", ctypes.c_int64)]
 
 
 class hegrid_plan_stats(ctypes.Structure):
@@ -58,7 +59,8 @@ class hegrid_plan_stats(ctypes.Structure):
                 ("nbr_max", ctypes.c_int32), ("nbr_mean", ctypes.c_double),
                 ("t_plan_ms", ctypes.c_double), ("nrow", ctypes.c_int32),
                 ("ncol", ctypes.c_int32), ("mlat", ctypes.c_int32), ("mlon", ctypes.c_int32),
-                ("sigma_deg", ctypes.c_double), ("radius_deg", ctypes.c_double)]
+                ("sigma_deg", ctypes.c_double), ("radius_deg", ctypes.c_double),
+                ("weight_image_bytes", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -87,6 +89,7 @@ SIGNATURES = {
     "hegrid_sort_u32": (I32, [P, I64, P, I32]),
     "hegrid_profile_enable": (I32, [PLAN, I32]),
     "hegrid_profile_read": (I32, [PLAN, P, P]),
+    "hegrid_pipeline_trace": (I32, [PLAN, P, I64, P]),
     "hegrid_launch_count": (I64, []),
     "hegrid_status_string": (ctypes.c_char_p, [I32]),
     "hegrid_abi_version": (I32, []),
@@ -143,8 +146,9 @@ def make_map(m) -> hegrid_map:
                       float(g("cdelt_lat")))
 
 
-def make_opts(device=0, n_streams=0, channel_block=0, engine=0) -> hegrid_opts:
-    return hegrid_opts(device, n_streams, channel_block, engine)
+def make_opts(device=0, n_streams=0, channel_block=0, engine=0,
+              weight_image_max_bytes=0) -> hegrid_opts:
+    return hegrid_opts(device, n_streams, channel_block, engine, weight_image_max_bytes)
 
 
 # ----------------------------------------------------------------- C-ABI names
@@ -238,6 +242,16 @@ def hegrid_profile_read(plan: int):
     _check(load().hegrid_profile_read(plan, ctypes.addressof(ms), ctypes.addressof(k)),
            "hegrid_profile_read")
     return ms.value, k.value
+
+
+def hegrid_pipeline_trace(plan: int) -> np.ndarray:
+    """[blocks][5] rows {slot, h2d_start, h2d_end, compute_end, d2h_end} (ms)."""
+    n = ctypes.c_int64()
+    _check(load().hegrid_pipeline_trace(plan, None, 0, ctypes.addressof(n)), "hegrid_pipeline_trace")
+    buf = np.zeros((n.value, 5), np.float64)
+    _check(load().hegrid_pipeline_trace(plan, _ptr(buf), n.value, ctypes.addressof(n)),
+           "hegrid_pipeline_trace")
+    return buf
 
 
 def hegrid_launch_count() -> int:

@@ -87,6 +87,20 @@ static hegrid_status create_common(const double* d_lon, const double* d_lat, int
     p->kern = *kernel;
     p->opts = o;
     p->n = n;
+    {   // the plan's stream-ordered pool (common.cuh): memory stays cached between calls
+        cudaMemPoolProps pp{};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = o.device;
+        cudaError_t e = cudaMemPoolCreate(&p->pool, &pp);
+        uint64_t keep = UINT64_MAX;
+        if (e == cudaSuccess) e = cudaMemPoolSetAttribute(p->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        if (e != cudaSuccess) {
+            if (p->pool) cudaMemPoolDestroy(p->pool);
+            delete p;
+            return cuda_status(e);
+        }
+    }
     hegrid_status s = build_plan(p, d_lon, d_lat, st);
     if (s != HEGRID_OK) {
         hegrid_plan_destroy(p);
@@ -175,13 +189,23 @@ void hegrid_plan_destroy(hegrid_plan_t p) {
     cudaFree(p->d_bin_start);
     cudaFree(p->d_mrow);
     cudaFree(p->d_cos_row);
-    cudaFree(p->d_scratch);
     cudaFree(p->d_tc_sched);
     cudaFree(p->d_tc_tile_off);
     cudaFree(p->d_tc_wsum);
     cudaFree(p->d_tc_wimg);
     cudaFree(p->d_tc_wslot);
     for (auto e : p->prof_events) cudaEventDestroy(e);
+    for (auto& x : p->slots) {
+        if (x.st) cudaStreamSynchronize(x.st);
+        for (auto e : x.ev)
+            if (e) cudaEventDestroy(e);
+        if (x.h_in) cudaFreeHost(x.h_in);
+        if (x.h_out) cudaFreeHost(x.h_out);
+        if (x.st) cudaStreamDestroy(x.st);
+    }
+    // outstanding stream-ordered allocations (none after the calls above) would defer the
+    // release to their frees
+    if (p->pool) cudaMemPoolDestroy(p->pool);
     delete p;
 }
 
@@ -204,6 +228,7 @@ hegrid_status hegrid_plan_info(hegrid_plan_t p, hegrid_plan_stats* out) {
     s.mlon = p->g.mlon;
     s.sigma_deg = p->g.sigma_rad / kDeg2Rad;
     s.radius_deg = p->g.R_rad / kDeg2Rad;
+    s.weight_image_bytes = p->tc_pw == 1 ? p->tc_wimg_bytes : 0;
     *out = s;
     return HEGRID_OK;
 }
@@ -250,8 +275,8 @@ static hegrid_status weights_only(hegrid_plan_s* p, float* d_w, cudaStream_t st)
     float* z = nullptr;
     float* o = nullptr;
     size_t nz = (size_t)std::max<int64_t>(p->n_used, 1) * 4;
-    HG_TRY(cudaMallocAsync(&z, nz * sizeof(float), st));
-    HG_TRY(cudaMallocAsync(&o, (size_t)p->g.nx * p->g.ny * sizeof(float), st));
+    HG_TRY(plan_alloc(p, &z, nz * sizeof(float), st));
+    HG_TRY(plan_alloc(p, &o, (size_t)p->g.nx * p->g.ny * sizeof(float), st));
     HG_TRY(cudaMemsetAsync(z, 0, nz * sizeof(float), st));
     hegrid_status s = launch_accumulate(p, z, 4, 1, o, d_w, st);
     cudaFreeAsync(z, st);
@@ -275,24 +300,24 @@ hegrid_status hegrid_grid_device(hegrid_plan_t p, const float* d_data, int64_t n
     }
     if (layout != HEGRID_LAYOUT_USER_CN) return HEGRID_EINVAL;
     if (ld < p->n) return HEGRID_EINVAL;
-    // USER_CN: permute channel blocks through a plan-layout scratch
+    // USER_CN: permute channel blocks through a plan-layout scratch, stream-ordered from the
+    // plan's pool on the caller's stream (no buffer shared between streams)
     int64_t cb = std::min<int64_t>(n_channels, 512);
     cb = (cb + 3) & ~3LL;
     size_t need = (size_t)std::max<int64_t>(p->n_used, 1) * cb * sizeof(float);
-    if (p->scratch_bytes < need) {
-        cudaFree(p->d_scratch);
-        p->d_scratch = nullptr;
-        p->scratch_bytes = 0;
-        HG_TRY(cudaMalloc(&p->d_scratch, need));
-        p->scratch_bytes = need;
-    }
-    for (int64_t c0 = 0; c0 < n_channels; c0 += cb) {
+    float* scratch = nullptr;
+    HG_TRY(plan_alloc(p, &scratch, need, st));
+    hegrid_status s = HEGRID_OK;
+    for (int64_t c0 = 0; c0 < n_channels && s == HEGRID_OK; c0 += cb) {
         int64_t cn = std::min(cb, n_channels - c0);
-        HG_TRY_S(launch_permute(p, d_data + c0 * ld, cn, ld, p->d_scratch, cb, st));
-        HG_TRY_S(accumulate_profiled(p, p->d_scratch, cb, cn, d_out + c0 * cells,
-                                     c0 == 0 ? d_weight : nullptr, st));
+        s = launch_permute(p, d_data + c0 * ld, cn, ld, scratch, cb, st);
+        if (s == HEGRID_OK)
+            s = accumulate_profiled(p, scratch, cb, cn, d_out + c0 * cells,
+                                    c0 == 0 ? d_weight : nullptr, st);
     }
-    return HEGRID_OK;
+    cudaError_t e = cudaFreeAsync(scratch, st);
+    if (s == HEGRID_OK) s = cuda_status(e);
+    return s;
 }
 
 hegrid_status hegrid_grid(hegrid_plan_t p, const float* data, int64_t n_channels,
@@ -303,16 +328,14 @@ hegrid_status hegrid_grid(hegrid_plan_t p, const float* data, int64_t n_channels
     HG_TRY(dg.err);
     const int64_t cells = (int64_t)p->g.nx * p->g.ny;
     const int64_t n = p->n;
-    float* d_w = nullptr;
-    if (weight_map) HG_TRY(cudaMalloc(&d_w, cells * sizeof(float)));
     if (n_channels == 0) {
-        hegrid_status s = HEGRID_OK;
-        if (weight_map) {
-            s = weights_only(p, d_w, 0);
-            if (s == HEGRID_OK)
-                s = cuda_status(cudaMemcpy(weight_map, d_w, cells * 4, cudaMemcpyDeviceToHost));
-            cudaFree(d_w);
-        }
+        if (!weight_map) return HEGRID_OK;
+        float* d_w = nullptr;
+        HG_TRY(plan_alloc(p, &d_w, cells * sizeof(float), 0));
+        hegrid_status s = weights_only(p, d_w, 0);
+        if (s == HEGRID_OK) s = cuda_status(cudaMemcpy(weight_map, d_w, cells * 4, cudaMemcpyDeviceToHost));
+        cudaFreeAsync(d_w, 0);
+        cudaStreamSynchronize(0);
         return s;
     }
     int64_t cb = p->opts.channel_block > 0 ? p->opts.channel_block
@@ -323,82 +346,125 @@ hegrid_status hegrid_grid(hegrid_plan_t p, const float* data, int64_t n_channels
     const int64_t nblk = (n_channels + cb - 1) / cb;
     const bool in_pinned = n == 0 || is_pinned(data);
     const bool out_pinned = is_pinned(out_map);
-    struct Slot {
-        cudaStream_t st = nullptr;
-        cudaEvent_t done = nullptr;
-        float *d_raw = nullptr, *d_v = nullptr, *d_out = nullptr;
-        float *h_in = nullptr, *h_out = nullptr;
-        int64_t pending = -1;   // block whose output waits in h_out
-    };
-    std::vector<Slot> sl(S);
+    const size_t raw_b = (size_t)cb * std::max<int64_t>(n, 1) * 4;
+    const size_t v_b = (size_t)cb * std::max<int64_t>(p->n_used, 1) * 4;
+    const size_t out_b = (size_t)cb * cells * 4;
     hegrid_status s = HEGRID_OK;
     auto fail = [&](cudaError_t e) {
         if (s == HEGRID_OK && e != cudaSuccess) s = cuda_status(e);
         return s != HEGRID_OK;
     };
-    const size_t raw_b = (size_t)cb * std::max<int64_t>(n, 1) * 4;
-    const size_t v_b = (size_t)cb * std::max<int64_t>(p->n_used, 1) * 4;
-    const size_t out_b = (size_t)cb * cells * 4;
-    for (int k = 0; k < S && s == HEGRID_OK; ++k) {
-        if (fail(cudaStreamCreateWithFlags(&sl[k].st, cudaStreamNonBlocking))) break;
-        if (fail(cudaEventCreateWithFlags(&sl[k].done, cudaEventDisableTiming))) break;
-        if (fail(cudaMalloc(&sl[k].d_raw, raw_b))) break;
-        if (fail(cudaMalloc(&sl[k].d_v, v_b))) break;
-        if (fail(cudaMalloc(&sl[k].d_out, out_b))) break;
-        if (!in_pinned && fail(cudaHostAlloc(&sl[k].h_in, raw_b, cudaHostAllocDefault))) break;
-        if (!out_pinned && fail(cudaHostAlloc(&sl[k].h_out, out_b, cudaHostAllocDefault))) break;
+    // the plan's staging slots (streams, events, pinned buffers) persist across calls
+    while ((int)p->slots.size() < S && s == HEGRID_OK) {
+        hegrid_plan_s::StageSlot x;
+        if (fail(cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking))) break;
+        for (auto& e : x.ev)
+            if (fail(cudaEventCreate(&e))) break;
+        p->slots.push_back(x);
     }
-    auto drain = [&](Slot& x) {
-        if (x.pending < 0) return;
-        if (fail(cudaEventSynchronize(x.done))) return;
+    auto grow = [&](float** h, size_t* cap, size_t need) {
+        if (*cap >= need) return;
+        if (*h) cudaFreeHost(*h);
+        *h = nullptr;
+        *cap = 0;
+        if (!fail(cudaHostAlloc(h, need, cudaHostAllocDefault))) *cap = need;
+    };
+    struct Dev {
+        float *raw = nullptr, *v = nullptr, *out = nullptr;
+        int64_t pending = -1;   // block whose output waits in the slot's pinned buffer
+    };
+    std::vector<Dev> dv(S);
+    for (int k = 0; k < S && s == HEGRID_OK; ++k) {
+        auto& x = p->slots[k];
+        if (!in_pinned) grow(&x.h_in, &x.in_cap, raw_b);
+        if (!out_pinned) grow(&x.h_out, &x.out_cap, out_b);
+        if (s != HEGRID_OK) break;
+        if (fail(plan_alloc(p, &dv[k].raw, raw_b, x.st))) break;
+        if (fail(plan_alloc(p, &dv[k].v, v_b, x.st))) break;
+        if (fail(plan_alloc(p, &dv[k].out, out_b, x.st))) break;
+    }
+    float* d_w = nullptr;
+    if (s == HEGRID_OK && weight_map) fail(plan_alloc(p, &d_w, cells * sizeof(float), p->slots[0].st));
+    // pipeline trace (profiling): four timing events per block on its slot's stream
+    const bool trace = p->profile;
+    std::vector<cudaEvent_t> tev;
+    if (trace && s == HEGRID_OK) {
+        tev.assign(4 * nblk, nullptr);
+        for (auto& e : tev)
+            if (fail(cudaEventCreate(&e))) break;
+    }
+    auto mark = [&](int64_t b, int k, cudaStream_t st) {
+        if (trace) fail(cudaEventRecord(tev[4 * b + k], st));
+    };
+    auto drain = [&](int k) {
+        Dev& d = dv[k];
+        if (d.pending < 0) return;
+        if (fail(cudaEventSynchronize(p->slots[k].ev[3]))) return;
         if (!out_pinned) {
-            int64_t c0 = x.pending * cb, cn = std::min(cb, n_channels - c0);
-            parallel_memcpy(out_map + c0 * cells, x.h_out, (size_t)cn * cells * 4);
+            int64_t c0 = d.pending * cb, cn = std::min(cb, n_channels - c0);
+            parallel_memcpy(out_map + c0 * cells, p->slots[k].h_out, (size_t)cn * cells * 4);
         }
-        x.pending = -1;
+        d.pending = -1;
     };
     for (int64_t b = 0; b < nblk && s == HEGRID_OK; ++b) {
-        Slot& x = sl[b % S];
-        drain(x);
+        const int k = (int)(b % S);
+        auto& x = p->slots[k];
+        Dev& d = dv[k];
+        drain(k);
         if (s != HEGRID_OK) break;
         const int64_t c0 = b * cb, cn = std::min(cb, n_channels - c0);
+        mark(b, 0, x.st);
         if (n > 0) {
             const float* src = data + c0 * n;
             if (!in_pinned) {
                 parallel_memcpy(x.h_in, src, (size_t)cn * n * 4);
                 src = x.h_in;
             }
-            if (fail(cudaMemcpyAsync(x.d_raw, src, (size_t)cn * n * 4, cudaMemcpyHostToDevice,
-                                     x.st)))
+            if (fail(cudaMemcpyAsync(d.raw, src, (size_t)cn * n * 4, cudaMemcpyHostToDevice, x.st)))
                 break;
-            if ((s = launch_permute(p, x.d_raw, cn, n, x.d_v, cb, x.st)) != HEGRID_OK) break;
+            mark(b, 1, x.st);
+            if ((s = launch_permute(p, d.raw, cn, n, d.v, cb, x.st)) != HEGRID_OK) break;
+        } else {
+            mark(b, 1, x.st);
         }
-        if ((s = launch_accumulate(p, x.d_v, cb, cn, x.d_out, b == 0 ? d_w : nullptr,
-                                        x.st)) != HEGRID_OK)
+        if ((s = launch_accumulate(p, d.v, cb, cn, d.out, b == 0 ? d_w : nullptr, x.st)) != HEGRID_OK)
             break;
+        mark(b, 2, x.st);
         float* dst = out_pinned ? out_map + c0 * cells : x.h_out;
-        if (fail(cudaMemcpyAsync(dst, x.d_out, (size_t)cn * cells * 4, cudaMemcpyDeviceToHost,
-                                 x.st)))
+        if (fail(cudaMemcpyAsync(dst, d.out, (size_t)cn * cells * 4, cudaMemcpyDeviceToHost, x.st)))
             break;
-        if (fail(cudaEventRecord(x.done, x.st))) break;
-        x.pending = b;
+        mark(b, 3, x.st);
+        if (fail(cudaEventRecord(x.ev[3], x.st))) break;
+        d.pending = b;
     }
-    for (auto& x : sl) drain(x);
+    for (int k = 0; k < S; ++k) drain(k);
     if (s == HEGRID_OK && weight_map) {
-        fail(cudaStreamSynchronize(sl[0].st));
+        fail(cudaStreamSynchronize(p->slots[0].st));
         if (s == HEGRID_OK) fail(cudaMemcpy(weight_map, d_w, cells * 4, cudaMemcpyDeviceToHost));
     }
-    for (auto& x : sl) {
-        if (x.st) cudaStreamSynchronize(x.st);
-        cudaFree(x.d_raw);
-        cudaFree(x.d_v);
-        cudaFree(x.d_out);
-        if (x.h_in) cudaFreeHost(x.h_in);
-        if (x.h_out) cudaFreeHost(x.h_out);
-        if (x.done) cudaEventDestroy(x.done);
-        if (x.st) cudaStreamDestroy(x.st);
+    for (int k = 0; k < S && k < (int)p->slots.size(); ++k) {
+        cudaStream_t st = p->slots[k].st;
+        if (dv[k].raw) cudaFreeAsync(dv[k].raw, st);
+        if (dv[k].v) cudaFreeAsync(dv[k].v, st);
+        if (dv[k].out) cudaFreeAsync(dv[k].out, st);
+        if (k == 0 && d_w) cudaFreeAsync(d_w, st);
+        cudaStreamSynchronize(st);
     }
-    if (d_w) cudaFree(d_w);
+    if (trace) {
+        p->trace.clear();
+        if (s == HEGRID_OK) {
+            for (int64_t b = 0; b < nblk; ++b) {
+                p->trace.push_back((double)(b % S));
+                for (int k = 0; k < 4; ++k) {
+                    float ms = 0;
+                    fail(cudaEventElapsedTime(&ms, tev[0], tev[4 * b + k]));
+                    p->trace.push_back(ms);
+                }
+            }
+        }
+        for (auto e : tev)
+            if (e) cudaEventDestroy(e);
+    }
     return s;
 }
 
@@ -409,7 +475,11 @@ hegrid_status hegrid_neighbours(hegrid_plan_t p, int64_t cell_begin, int64_t cel
     if (cell_begin < 0 || cell_end < cell_begin || cell_end > cells) return HEGRID_EINVAL;
     DeviceGuard dg(p->device);
     HG_TRY(dg.err);
-    return plan_neighbours(p, cell_begin, cell_end, offsets, sample_idx, 0);
+    // the pairs of the engine that grids: the tensor-core engine's chunk schedule (the
+    // default), or the SIMT engine's per-cell candidate ranges
+    if (p->opts.engine == HEGRID_ENGINE_SIMT)
+        return plan_neighbours(p, cell_begin, cell_end, offsets, sample_idx, 0);
+    return tc_neighbours(p, cell_begin, cell_end, offsets, sample_idx, 0);
 }
 
 hegrid_status hegrid_sort_u32(const uint32_t* keys, int64_t n, int32_t* perm, int32_t device) {
@@ -431,6 +501,16 @@ hegrid_status hegrid_sort_u32(const uint32_t* keys, int64_t n, int32_t* perm, in
     cudaFree(dk);
     if (dv) cudaFree(dv);
     return s;
+}
+
+hegrid_status hegrid_pipeline_trace(hegrid_plan_t p, double* buf, int64_t cap_rows,
+                                    int64_t* n_rows) {
+    if (!p || cap_rows < 0) return HEGRID_EINVAL;
+    const int64_t rows = (int64_t)p->trace.size() / 5;
+    if (n_rows) *n_rows = rows;
+    if (buf)
+        for (int64_t i = 0; i < std::min(rows, cap_rows) * 5; ++i) buf[i] = p->trace[i];
+    return HEGRID_OK;
 }
 
 hegrid_status hegrid_profile_enable(hegrid_plan_t p, int32_t enable) {

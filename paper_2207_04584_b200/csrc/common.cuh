@@ -17,6 +17,9 @@ inline void count_launch(int k = 1) { g_launches.fetch_add(k, std::memory_order_
 
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kDeg2Rad = kPi / 180.0;
+// largest half-longitude offset (rad) of a pair within R that the fp32 series distance
+// serves (weight.cuh sin2_series; make_geom refuses wider reaches)
+constexpr double kMaxHalfDlon = 0.5;
 
 // Geometry of the bin index and kernel, passed by value to kernels.
 // Bin (br, bc) of the index covers the cell-sized box around cell (bc - mlon, br - mlat);
@@ -89,11 +92,27 @@ struct hegrid_plan_s {
     // blocks' tf32 hi then lo weights in the shared-memory operand layout (4 KB per block)
     mutable uint8_t* d_tc_wimg = nullptr;
     mutable uint32_t* d_tc_wslot = nullptr;    // [entries] first 4-KB slot of each entry
-    mutable int tc_pw = -1;                    // -1 not built, 0 unavailable, 1 built
+    mutable int tc_pw = -1;                    // -1 not built (retried on later calls), 1 built
     mutable int64_t tc_wimg_bytes = 0;
-    // scratch for USER_CN device grids
-    float* d_scratch = nullptr;
-    size_t scratch_bytes = 0;
+    // Stream-ordered device memory pool of the plan (the paper's per-stream "memory pool",
+    // PAPER.md:315-316): every per-call device buffer (USER_CN scratch, split-tile partial
+    // sums, non-finite records, hegrid_grid's channel-block slots) is taken from it on the
+    // caller's stream and returned to it on the same stream, so calls on different streams
+    // never share a buffer and repeated calls reuse the memory (release threshold: never).
+    cudaMemPool_t pool = nullptr;
+    // hegrid_grid's staging slots, created on first use and reused by later calls: one CUDA
+    // stream, its events and pinned host buffers (grown on demand) per slot
+    struct StageSlot {
+        cudaStream_t st = nullptr;
+        cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};   // h2d start/end, compute end, d2h end
+        float* h_in = nullptr;
+        float* h_out = nullptr;
+        size_t in_cap = 0, out_cap = 0;
+    };
+    std::vector<StageSlot> slots;
+    // pipeline trace of the last hegrid_grid call (profiling on): per channel block
+    // {slot, t_h2d_start, t_h2d_end, t_compute_end, t_d2h_end} (ms from the first event)
+    std::vector<double> trace;
 
     hg::PlanDev dev() const {
         return hg::PlanDev{d_geo, d_ll, d_bin_start, d_mrow, d_cos_row};
@@ -119,6 +138,8 @@ hegrid_status launch_accumulate_simt(const hegrid_plan_s* p, const float* d_v, i
 hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int64_t ldv,
                                    int64_t n_channels, float* d_out, float* d_weight,
                                    cudaStream_t st);
+hegrid_status tc_neighbours(const hegrid_plan_s* p, int64_t c0, int64_t c1, int64_t* offsets,
+                            int64_t* idx, cudaStream_t st);
 // engine dispatch (api.cu)
 hegrid_status launch_accumulate(const hegrid_plan_s* p, const float* d_v, int64_t ldv,
                                 int64_t n_channels, float* d_out, float* d_weight,
@@ -126,6 +147,10 @@ hegrid_status launch_accumulate(const hegrid_plan_s* p, const float* d_v, int64_
 // permute.cu
 hegrid_status launch_permute(const hegrid_plan_s* p, const float* d_user, int64_t n_channels,
                              int64_t ld_user, float* d_plan, int64_t ld_plan, cudaStream_t st);
+
+inline cudaError_t plan_alloc(const hegrid_plan_s* p, void* ptr, size_t bytes, cudaStream_t st) {
+    return cudaMallocFromPoolAsync(reinterpret_cast<void**>(ptr), bytes, p->pool, st);
+}
 
 inline hegrid_status cuda_status(cudaError_t e) {
     if (e == cudaSuccess) return HEGRID_OK;

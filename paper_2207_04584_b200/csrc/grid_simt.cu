@@ -18,6 +18,7 @@
 //   Epilogue: V = S / W (IEEE div.rn), NaN where W = 0, transposed through shared memory
 //   so out_map[c][j][i] rows are written as whole 32-byte sectors.
 #include "common.cuh"
+#include "nonfinite.cuh"
 #include "weight.cuh"
 
 namespace hg {
@@ -30,8 +31,12 @@ __device__ __forceinline__ float4 ldg_nc(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
+// One sample's QC channel values.  Non-finite values (nonfinite.cuh) are zeroed, so they
+// cannot reach the warp block's other cells through 0 * NaN, and recorded (plan position
+// `pos`, channel c0 + q) for the fix-up; channels >= C are never recorded.
 template <int QC>
-__device__ __forceinline__ void load_row(const float* p, bool ok, float* v) {
+__device__ __forceinline__ void load_row(const float* p, bool ok, float* v, uint32_t pos, int c0,
+                                         int C, NfBuf nf) {
 #pragma unroll
     for (int q4 = 0; q4 < QC; q4 += 4) {
         float4 x = ok ? ldg_nc(p + q4) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -40,6 +45,17 @@ __device__ __forceinline__ void load_row(const float* p, bool ok, float* v) {
         v[q4 + 2] = x.z;
         v[q4 + 3] = x.w;
     }
+    float s = 0.0f;
+#pragma unroll
+    for (int q = 0; q < QC; ++q) s += v[q];
+    if (nf_bad(s)) {
+#pragma unroll
+        for (int q = 0; q < QC; ++q)
+            if (nf_bad(v[q])) {
+                v[q] = 0.0f;
+                if (c0 + q < C) nf_record(nf, pos, (uint32_t)(c0 + q));
+            }
+    }
 }
 
 template <int QC, bool SPLIT>
@@ -47,7 +63,7 @@ __global__ void __launch_bounds__(SIMT_THREADS, (QC == 4 && !SPLIT) ? 2 : 1) k_a
                                                              const float* __restrict__ V,
                                                              int64_t ldv, int C,
                                                              float* __restrict__ out,
-                                                             float* __restrict__ wout) {
+                                                             float* __restrict__ wout, NfBuf nf) {
     constexpr int CB = 32 * QC;
     constexpr int SO = TW * TH + 1;                 // padded row of the epilogue tile
     __shared__ float4 wbuf[SIMT_THREADS / 32][32][2];
@@ -133,7 +149,7 @@ __global__ void __launch_bounds__(SIMT_THREADS, (QC == 4 && !SPLIT) ? 2 : 1) k_a
                 if (mask) {
                     tn = __ffs(mask) - 1;
                     mask &= mask - 1;
-                    load_row<QC>(V + (int64_t)(base + tn) * ldv + c_lane, ch_ok, vn);
+                    load_row<QC>(V + (int64_t)(base + tn) * ldv + c_lane, ch_ok, vn, base + tn, c_lane, C, nf);
                 }
                 while (tn >= 0) {
                     const int t = tn;
@@ -144,7 +160,7 @@ __global__ void __launch_bounds__(SIMT_THREADS, (QC == 4 && !SPLIT) ? 2 : 1) k_a
                     if (mask) {
                         tn = __ffs(mask) - 1;
                         mask &= mask - 1;
-                        load_row<QC>(V + (int64_t)(base + tn) * ldv + c_lane, ch_ok, vn);
+                        load_row<QC>(V + (int64_t)(base + tn) * ldv + c_lane, ch_ok, vn, base + tn, c_lane, C, nf);
                     }
                     const float4 wa = wbuf[warp][t][0], wb = wbuf[warp][t][1];
                     const float ww[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
@@ -212,9 +228,12 @@ static hegrid_status launch_qc(const hegrid_plan_s* p, const float* d_v, int64_t
     size_t smem = sizeof(float) * (32 * QC) * (TW * TH + 1);
     HG_TRY(cudaFuncSetAttribute(k_accum_simt<QC, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
-    k_accum_simt<QC, SPLIT><<<grid, SIMT_THREADS, smem, st>>>(g, p->dev(), d_v, ldv, C, d_out, d_w);
+    NfBuf nf;
+    HG_TRY_S(nonfinite_alloc(p, &nf, st));
+    k_accum_simt<QC, SPLIT><<<grid, SIMT_THREADS, smem, st>>>(g, p->dev(), d_v, ldv, C, d_out, d_w, nf);
     count_launch();
-    return cuda_status(cudaGetLastError());
+    HG_TRY(cudaGetLastError());
+    return nonfinite_fix(p, d_v, ldv, C, nf, d_out, st);
 }
 
 hegrid_status launch_accumulate_simt(const hegrid_plan_s* p, const float* d_v, int64_t ldv,

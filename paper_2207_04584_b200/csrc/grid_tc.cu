@@ -37,6 +37,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <chrono>
 #include <type_traits>
 #include <vector>
@@ -45,6 +46,7 @@
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
+#include "nonfinite.cuh"
 #include "weight.cuh"
 
 namespace hg {
@@ -371,6 +373,57 @@ __global__ void k_tc_wsum(const __grid_constant__ Geom g, PlanDev pd, float* __r
     wsum[cell] = W;
 }
 
+// Neighbour export through the tensor-core engine's own pairs: one CTA per tile walks the
+// tile's schedule entries and, for every (in-reach block, cell row, sample quad) item,
+// computes the 4 x 4 weights with patch_weights -- the expression entry_weights uses for
+// the B operand and k_tc_wsum for W -- and emits (cell, original index) for every w > 0 whose
+// cell lies in [c0, c1).  A pair the schedule prunes is therefore missing here exactly as it
+// is missing from the maps (Algorithm 1's gather set).
+// idx == nullptr: count into cnt[cell - c0]; else fill idx[off[cell - c0] + cursor].
+__global__ void __launch_bounds__(128)
+k_tc_pairs(const __grid_constant__ Geom g, PlanDev pd, const int32_t* __restrict__ perm,
+           const uint4* __restrict__ sched, const uint32_t* __restrict__ tile_off, int64_t c0,
+           int64_t c1, unsigned long long* __restrict__ cnt, const int64_t* __restrict__ off,
+           int64_t* __restrict__ idx) {
+    const int tiles_x = (g.nx + TC_TW - 1) / TC_TW;
+    const int i0 = (blockIdx.x % tiles_x) * TC_TW, j0 = (blockIdx.x / tiles_x) * TC_TH;
+    {   // skip tiles with no cell in [c0, c1)
+        bool any = false;
+        const int i1 = min(i0 + TC_TW, g.nx) - 1;
+        for (int j = j0; j < min(j0 + TC_TH, g.ny) && !any; ++j)
+            any = (int64_t)j * g.nx + i1 >= c0 && (int64_t)j * g.nx + i0 < c1;
+        if (!any) return;
+    }
+    for (uint32_t ei = tile_off[blockIdx.x]; ei < tile_off[blockIdx.x + 1]; ++ei) {
+        const uint4 e = __ldg(&sched[ei]);
+        const uint32_t pstart = e.x, nk = e.y & 255;
+        const int row = (int)(e.y >> 8), nq = __popc(e.z);
+        for (int it = threadIdx.x; it < nq * 4 * (TC_KC / 4); it += blockDim.x) {
+            const int kq = it % (TC_KC / 4), rr = (it / (TC_KC / 4)) & 3, q = it / TC_KC;
+            const int b = (e.w >> (4 * q)) & 15;
+            const int cj = j0 + (b / TC_BX) * 4 + rr, ci0 = i0 + (b % TC_BX) * 4;
+            if (cj >= g.ny) continue;
+            float4 s[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                s[u] = (uint32_t)(4 * kq + u) < nk ? __ldg(&pd.geo[pstart + 4 * kq + u])
+                                                  : make_float4(0.0f, kInvalidDy, 0.0f, 0.0f);
+            float w[4][4];
+            patch_weights<4>(g, pd, row, cj, ci0, 0, __ldg(&pd.cos_row[cj]), s, pstart + 4 * kq, w);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int64_t cell = (int64_t)cj * g.nx + ci0 + c;
+                    if (w[u][c] > 0.0f && cell >= c0 && cell < c1) {
+                        const unsigned long long k = atomicAdd(&cnt[cell - c0], 1ull);
+                        if (idx) idx[off[cell - c0] + (int64_t)k] = perm[pstart + 4 * kq + u];
+                    }
+                }
+        }
+    }
+}
+
 // The weight image (PW mode): one CTA of 256 threads per tile walks the tile's entries; the
 // threads compute the B-producer items of each entry (entry_weights) into global memory at
 // the entry's slots: [nq x 2 KB hi][nq x 2 KB lo], byte-identical to the shared-memory stage.
@@ -410,14 +463,25 @@ static void prep_mark(const char* what) {
     t0 = t;
 }
 
+// The image's size is known from the schedule statistics ((chunk, block) pairs = B slots),
+// so the budget check is cheap and a plan whose image did not fit retries on later calls
+// (hegrid_opts.weight_image_max_bytes: 0 = 1/4 of the free device memory, > 0 = a byte cap,
+// < 0 = never).
 static bool ensure_tc_wimage(const hegrid_plan_s* p, cudaStream_t st) {
-    if (p->tc_pw >= 0) return p->tc_pw == 1;
-    p->tc_pw = 0;
+    if (p->tc_pw == 1) return true;
+    const int64_t cap = p->opts.weight_image_max_bytes;
+    if (cap < 0) return false;
+    const int64_t ne = p->tc_nchunks;
+    if (ne <= 0) return false;
+    {
+        const uint64_t want = (uint64_t)p->tc_stats[1] * 2u * SLOT_BYTES;
+        size_t fr = 0, total = 0;
+        if (cudaMemGetInfo(&fr, &total) != cudaSuccess) return false;
+        if (want > (cap > 0 ? (uint64_t)cap : fr / 4) || want > fr) return false;
+    }
     prep_mark("wimage start");
     const Geom& g = p->g;
     const int tiles = ((g.nx + TC_TW - 1) / TC_TW) * ((g.ny + TC_TH - 1) / TC_TH);
-    const int64_t ne = p->tc_nchunks;
-    if (ne <= 0) return false;
     std::vector<uint4> h(ne);
     if (cudaMemcpyAsync(h.data(), p->d_tc_sched, ne * sizeof(uint4), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
@@ -430,8 +494,7 @@ static bool ensure_tc_wimage(const hegrid_plan_s* p, cudaStream_t st) {
         tot += (uint64_t)__builtin_popcount(h[i].z);
     }
     const uint64_t bytes = tot * 2u * SLOT_BYTES;
-    size_t fr = 0, total = 0;
-    if (tot >= (1ull << 32) || cudaMemGetInfo(&fr, &total) != cudaSuccess || bytes > fr / 4) return false;
+    if (tot >= (1ull << 32)) return false;
     uint8_t* d_img = nullptr;
     uint32_t* d_slot = nullptr;
     prep_mark("slot scan + meminfo");
@@ -543,7 +606,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
            const uint8_t* __restrict__ wimg, const uint32_t* __restrict__ wslot,
            int C, int tiles, int cgroup, int super_, int snake, int nsplit,
            float* __restrict__ part, float* __restrict__ out,
-           float* __restrict__ wout, int dbg_in) {
+           float* __restrict__ wout, NfBuf nf, int dbg_in) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmem& sm = *reinterpret_cast<TcSmem*>(smem_raw);
     if (tc::smem_u32(smem_raw) & 1023u) __trap();   // swizzle atoms need 1024-B alignment
@@ -744,6 +807,16 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 const uint32_t a0 = tmem + A_COL0 + sa * 2 * TC_KC;
                 const uint32_t dbase = tmem + (uint32_t)d * D_COLS;
                 uint32_t mm = mask & rows;
+                if (dbg & 65536) {
+                    // what-if (profiling builds): one run of N = 16 * ((dbg >> 17) & 15)
+                    // cells per entry, issued by issuer 0 (timing only; results garbage)
+                    mm = 0;
+                    if (issuer == 0) {
+                        const int nw = 16 * ((dbg >> 17) & 15);
+                        tc::mma12_3xtf32<(32 >> 4), TC_KC>(dbase, a0, dh0, dh0 + (uint32_t)lo16,
+                                                           tc::idesc_tf32(TC_M, nw));
+                    }
+                }
 #if defined(HG_TC_MMA36)
                 static_assert(KA == 1, "36-MMA issue for 32-sample chunks");
                 while (mm) {                       // up to three runs per asm block
@@ -977,16 +1050,35 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             }
             // The values now live in registers: release the value stage (the V loader refills
             // it while this chunk still waits for its A stage).  An mbarrier arrive does not
-            // wait for outstanding shared loads, so a store of the xor of every split result
-            // (which cannot issue before all loads returned) goes first.
-            uint32_t dep = ee.x ^ ee.y ^ ee.z;
+            // wait for outstanding shared loads, so a store of a value that depends on every
+            // loaded word goes first: the sum of the lo parts (lo = v - hi depends on v).
+            float s0 = 0.0f, s1 = 0.0f;
 #pragma unroll
-            for (int k = 0; k < KPW; ++k) dep ^= lo[k] ^ hi[k];
+            for (int k = 0; k < KPW; k += 2) {
+                s0 += __uint_as_float(lo[k]);
+                s1 += __uint_as_float(lo[k + 1]);
+            }
+            const float lsum = s0 + s1;
+            const uint32_t dep = ee.x ^ ee.y ^ ee.z ^ __float_as_uint(lsum);
             if (warp == 4 && lane == 0 && tl_on && c < 256) g_tl[c][8] = clock64() + (dep == 0x12345u);
             asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[warp])), "r"(dep) : "memory");
             // one arrive per warp (hundreds of per-thread arrives on one mbarrier serialise)
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&sm.v_empty[sv]);
+            // Non-finite values (nonfinite.cuh): lo is NaN / Inf iff v is non-finite (or
+            // beyond the tf32 range), so the same sum flags them.  Such a value is zeroed
+            // here -- it cannot poison the block's other cells through 0 * NaN -- and
+            // recorded for the fix-up, which applies it to exactly the cells within its
+            // support.  (Unrolled: hi / lo must stay in registers.)
+            if (nf_bad(lsum)) {
+#pragma unroll
+                for (int k = 0; k < KPW; ++k) {
+                    if (!nf_bad(__uint_as_float(lo[k]))) continue;
+                    hi[k] = 0u;
+                    lo[k] = 0u;
+                    if ((uint32_t)(k0 + k) < nk && cb + chl < C) nf_record(nf, ee.x + k0 + k, cb + chl);
+                }
+            }
         };
         auto store = [&](int c) {
             const int sa = c % NA;
@@ -1237,7 +1329,7 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     dim3 grid(tiles * ncb * nsplit);
     float* d_part = nullptr;
     if (nsplit > 1)
-        HG_TRY(cudaMallocAsync(&d_part, (size_t)nsplit * C * (size_t)g.nx * g.ny * sizeof(float), st));
+        HG_TRY(plan_alloc(p, &d_part, (size_t)nsplit * C * (size_t)g.nx * g.ny * sizeof(float), st));
     size_t smem = sizeof(TcSmem);
     int dbg = 0;
     if (const char* e = getenv("HEGRID_TC_DEBUG")) dbg = atoi(e);
@@ -1259,9 +1351,11 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     auto kern = pw ? (sparse ? k_accum_tc<SEG_SPARSE, true> : k_accum_tc<SEG_DENSE, true>)
                    : (sparse ? k_accum_tc<SEG_SPARSE, false> : k_accum_tc<SEG_DENSE, false>);
     HG_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NfBuf nf;
+    HG_TRY_S(nonfinite_alloc(p, &nf, st));
     kern<<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched, p->d_tc_tile_off,
                                          p->d_tc_wsum, p->d_tc_wimg, p->d_tc_wslot, C, tiles, cgroup,
-                                         super_, snake, nsplit, d_part, d_out, d_weight, dbg);
+                                         super_, snake, nsplit, d_part, d_out, d_weight, nf, dbg);
     count_launch();
     if (nsplit > 1) {
         const int64_t n = (int64_t)C * g.nx * g.ny;
@@ -1270,6 +1364,7 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
         count_launch();
         cudaFreeAsync(d_part, st);
     }
+    HG_TRY_S(nonfinite_fix(p, d_v, ldv, C, nf, d_out, st));
     if (dbg & 32) {
         unsigned long long h[16];
         cudaStreamSynchronize(st);
@@ -1299,6 +1394,57 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
         }
     }
     return cuda_status(cudaGetLastError());
+}
+
+}  // namespace hg
+
+namespace hg {
+
+// hegrid_neighbours for the tensor-core engine: the CSR of cells [c0, c1) from k_tc_pairs
+// (count pass, host scan, fill pass), each cell's list sorted by original index.
+hegrid_status tc_neighbours(const hegrid_plan_s* p, int64_t c0, int64_t c1, int64_t* offsets,
+                            int64_t* idx, cudaStream_t st) {
+    const int64_t nc = c1 - c0;
+    offsets[0] = 0;
+    if (nc == 0) return HEGRID_OK;
+    HG_TRY_S(ensure_tc_plan(p, st));
+    const Geom& g = p->g;
+    const int tiles = ((g.nx + TC_TW - 1) / TC_TW) * ((g.ny + TC_TH - 1) / TC_TH);
+    unsigned long long* d_cnt = nullptr;
+    int64_t *d_off = nullptr, *d_idx = nullptr;
+    std::vector<unsigned long long> h(nc);
+    cudaError_t e = cudaMalloc(&d_cnt, nc * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_cnt, 0, nc * sizeof(unsigned long long), st);
+    if (e == cudaSuccess && p->n_used > 0) {
+        k_tc_pairs<<<tiles, 128, 0, st>>>(g, p->dev(), p->d_perm, p->d_tc_sched, p->d_tc_tile_off,
+                                          c0, c1, d_cnt, nullptr, nullptr);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d_cnt, nc * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    for (int64_t q = 0; q < nc && e == cudaSuccess; ++q) offsets[q + 1] = offsets[q] + (int64_t)h[q];
+    const int64_t tot = offsets[nc];
+    if (e == cudaSuccess && idx && tot > 0) {
+        e = cudaMalloc(&d_off, nc * sizeof(int64_t));
+        if (e == cudaSuccess) e = cudaMalloc(&d_idx, tot * sizeof(int64_t));
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_off, offsets, nc * 8, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(d_cnt, 0, nc * sizeof(unsigned long long), st);
+        if (e == cudaSuccess) {
+            k_tc_pairs<<<tiles, 128, 0, st>>>(g, p->dev(), p->d_perm, p->d_tc_sched,
+                                              p->d_tc_tile_off, c0, c1, d_cnt, d_off, d_idx);
+            count_launch();
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(idx, d_idx, tot * 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess)
+            for (int64_t q = 0; q < nc; ++q) std::sort(idx + offsets[q], idx + offsets[q + 1]);
+    }
+    cudaFree(d_cnt);
+    if (d_off) cudaFree(d_off);
+    if (d_idx) cudaFree(d_idx);
+    return cuda_status(e);
 }
 
 }  // namespace hg

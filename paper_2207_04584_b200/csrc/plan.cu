@@ -270,6 +270,10 @@ static hegrid_status make_geom(hegrid_plan_s* p, std::vector<int>& mrow,
         Amax = std::max(Amax, A);
         mrow[br] = (int)floor(A / adlon + 0.5 + eps);
     }
+    // the fp32 hot-path distance keeps sin^2(dlon/2)'s series through b^8 (weight.cuh):
+    // accurate to < 6e-7 for half-longitude offsets b <= 0.5 rad; beyond (fields within a
+    // degree or two of a pole) the lon/lat bin index is not used
+    if (0.5 * Amax * kDeg2Rad > kMaxHalfDlon) return HEGRID_EUNSUPPORTED;
     g.mlon = 0;
     for (int v : mrow) g.mlon = std::max(g.mlon, v);
     // longitude: no wrap ambiguity between the crval frame and the cell frame

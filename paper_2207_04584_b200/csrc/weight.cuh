@@ -7,8 +7,11 @@
 //     h = sin^2(dlat/2) + cos(lat_c) cos(lat_s) sin^2(dlon/2),   d^2 = 4 asin^2(sqrt h)
 // evaluated by series on exact small offsets: dlat/dlon are (integer bin-to-cell offset +
 // the sample's fp32 offset from its bin centre) x cdelt, so no large absolute angles are
-// ever rounded to fp32.  Truncation of the series is < 3e-7 relative for R <= 1 deg
-// (plan-enforced).  The support test is decided in fp32 outside a +-1e-5 relative guard
+// ever rounded to fp32.  Near a pole, pairs within R have half-longitude offsets b of up to
+// tens of degrees, so sin^2(b) keeps its series up to the b^8 term (sin2_series): the
+// truncation 2 b^10 / 14175 is < 6e-7 relative for b <= kMaxHalfDlon = 0.5 rad, which the
+// plan enforces (make_geom: EUNSUPPORTED beyond; HEALPix engine territory).  sin^2(dlat/2)
+// keeps two terms: dlat <= R <= 1 deg, truncation < 3e-10.  The support test is decided in fp32 outside a +-1e-5 relative guard
 // band around R^2 and re-decided inside it by an fp64 haversine on the original fp64
 // coordinates, written out without FMA contraction, so the neighbour set is the fp64 one.
 #pragma once
@@ -16,6 +19,17 @@
 #include "common.cuh"
 
 namespace hg {
+
+// sin^2(b) by its Taylor series through b^8 (relative truncation 2 b^8 / 14175: 5.5e-7 at
+// b = 0.5 rad).  |b| is clamped to 1.5 rad, below the polynomial's first maximum (b = 1.55),
+// so the result stays increasing in |b| and a far pair (beyond any support) never looks near.
+__device__ __forceinline__ float sin2_series(float b) {
+    b = fminf(fabsf(b), 1.5f);
+    const float x = __fmul_rn(b, b);
+    float q = fmaf(x, -1.0f / 315.0f, 2.0f / 45.0f);
+    q = fmaf(x, q, -1.0f / 3.0f);
+    return fmaf(__fmul_rn(x, q), x, x);
+}
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -61,9 +75,9 @@ __device__ __forceinline__ float pair_d2(const Geom& g, float dx_cells, float dy
                                          float cc) {
     float a = dy_cells * (0.5f * g.dlat_rad);
     float b = dx_cells * (0.5f * g.dlon_rad);
-    float a2 = a * a, b2 = b * b;
+    float a2 = a * a;
     float sa = a2 * (1.0f - a2 * (1.0f / 3.0f));   // sin^2(dlat/2)
-    float sb = b2 * (1.0f - b2 * (1.0f / 3.0f));   // sin^2(dlon/2)
+    float sb = sin2_series(b);                     // sin^2(dlon/2)
     float h = sa + cc * sb;
     return 4.0f * h * (1.0f + h * ((1.0f / 3.0f) + h * (8.0f / 45.0f)));  // 4 asin^2(sqrt h)
 }
@@ -103,47 +117,38 @@ template <int NCOL>
 __device__ __forceinline__ void patch_weights(const Geom& g, const PlanDev& pd, int br, int cj,
                                               int ci0, int c0, float cos_c, const float4 (&s)[4],
                                               uint32_t p0, float (&w)[4][NCOL]) {
-    const float hlon = 0.5f * g.dlon_rad, hlat = 0.5f * g.dlat_rad;
+    // Every operation is an explicitly rounded intrinsic or fmaf: no FMA contraction is left
+    // to the compiler, so each instantiation (NCOL, c0, inlining context) produces the same
+    // bits for the same (cell, sample) -- the B operand, W and the neighbour export must
+    // agree pair by pair (a contraction difference once moved a pair 1.8e-7 outside the guard
+    // band in one of them).
+    const float hlon = __fmul_rn(0.5f, g.dlon_rad), hlat = __fmul_rn(0.5f, g.dlat_rad);
     const float fy = (float)(br - g.mlat - cj);
     const int ix = -g.mlon - ci0;
-    uint32_t kill = 0;      // bit NCOL u + j: band pair outside the fp64 support
     // exponent t = neg_k2 * d^2 with d^2 = 4 asin^2(sqrt h) = h (4 + 4h/3 + 32h^2/45 + ...)
-    bool band = false;      // some pair inside the guard band
+    uint32_t band = 0;      // bit NCOL u + j: pair inside the guard band
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-        const float a = fminf(fabsf((fy + s[u].y) * hlat), 1.0f);
-        const float a2 = a * a;
-        const float sa = fmaf(a2 * (-1.0f / 3.0f), a2, a2);
-        const float ccs = cos_c * s[u].z;
-        const float b0 = ((float)(__float_as_int(s[u].w) + ix) + s[u].x) * hlon;
+        const float a = fminf(fabsf(__fmul_rn(__fadd_rn(fy, s[u].y), hlat)), 1.0f);
+        const float a2 = __fmul_rn(a, a);
+        const float sa = fmaf(__fmul_rn(a2, -1.0f / 3.0f), a2, a2);
+        const float ccs = __fmul_rn(cos_c, s[u].z);
+        const float b0 = __fmul_rn(__fadd_rn((float)(__float_as_int(s[u].w) + ix), s[u].x), hlon);
 #pragma unroll
         for (int j = 0; j < NCOL; ++j) {
-            const float bb = b0 - (float)(c0 + j) * hlon;
-            const float b2 = bb * bb;
-            const float sbv = fmaf(b2 * (-1.0f / 3.0f), b2, b2);
+            const float sbv = sin2_series(__fsub_rn(b0, __fmul_rn((float)(c0 + j), hlon)));
             const float h = fmaf(ccs, sbv, sa);
-            const float t = h * fmaf(h, fmaf(h, g.tK2, g.tK1), g.tK0);
-            band |= (t < g.t_in) & (t >= g.t_out);
-            w[u][j] = t >= g.t_out ? ex2_approx(t * g.wexp) : 0.0f;   // band pairs provisionally in
+            const float t = __fmul_rn(h, fmaf(h, fmaf(h, g.tK2, g.tK1), g.tK0));
+            band |= (uint32_t)((t < g.t_in) & (t >= g.t_out)) << (u * NCOL + j);
+            w[u][j] = t >= g.t_out ? ex2_approx(__fmul_rn(t, g.wexp)) : 0.0f;   // band pairs provisionally in
         }
     }
-    if (band) {   // rare: find the guard-band pairs again and decide them in fp64
+    if (band) {   // rare: decide the guard-band pairs (flagged above) in fp64
+        uint32_t kill = 0;
 #pragma unroll 1
-        for (int k = 0; k < 4 * NCOL; ++k) {
-            const int u = k / NCOL, cc = c0 + k % NCOL;
-            // (selects, not s[u]: a dynamic index would put s in local memory)
-            const float4 su = u == 0 ? s[0] : (u == 1 ? s[1] : (u == 2 ? s[2] : s[3]));
-            const float a = fminf(fabsf((fy + su.y) * hlat), 1.0f);
-            const float a2 = a * a;
-            const float sa = fmaf(a2 * (-1.0f / 3.0f), a2, a2);
-            const float ccs = cos_c * su.z;
-            const float b0 = ((float)(__float_as_int(su.w) + ix) + su.x) * hlon;
-            const float bb = b0 - (float)cc * hlon;
-            const float b2 = bb * bb;
-            const float sbv = fmaf(b2 * (-1.0f / 3.0f), b2, b2);
-            const float h = fmaf(ccs, sbv, sa);
-            const float t = h * fmaf(h, fmaf(h, g.tK2, g.tK1), g.tK0);
-            if (t < g.t_in && t >= g.t_out && ci0 + cc < g.nx) {
+        for (uint32_t m = band; m; m &= m - 1) {
+            const int k = __ffs(m) - 1, u = k / NCOL, cc = c0 + k % NCOL;
+            if (ci0 + cc < g.nx) {
                 const double2 ll = pd.ll[p0 + u];
                 if (!support_fp64(g, ci0 + cc, cj, ll.x, ll.y)) kill |= 1u << k;
             }

@@ -76,3 +76,26 @@ def engine_env(engine, monkeypatch):
         monkeypatch.setenv("HEGRID_TC_SNAKE", "1")
         return "tc"
     return engine
+
+
+def compare_scaled(out_gpu, w_gpu, lon, lat, vals, m, fwhm, support=3.0, rtol=RTOL, cells=None,
+                   kernel="gaussian"):
+    """Scale-aware parity for values of any sign: on covered cells,
+    |V_gpu - V_ora| <= rtol * (sum_n w |v_n|) / W -- the error of a weighted mean whose terms
+    each carry relative error rtol -- plus the W and blank-pattern rules of ``compare``.
+    ``vals`` [C][N]; returns the statistics."""
+    o, Wo, _ = oracle.grid(lon, lat, vals, m, fwhm, support, cells=cells, kernel=kernel)
+    oa, _, _ = oracle.grid(lon, lat, np.abs(np.asarray(vals, np.float32)), m, fwhm, support,
+                           cells=cells, kernel=kernel)
+    out_gpu = np.asarray(out_gpu, np.float64).reshape(o.shape)
+    w_gpu = np.asarray(w_gpu, np.float64).reshape(Wo.shape)
+    cov = Wo > 0
+    assert np.array_equal(w_gpu > 0, cov), "blank pattern differs"
+    assert np.all(np.isnan(out_gpu[:, ~cov]))
+    werr = np.abs(w_gpu[cov] - Wo[cov]) / Wo[cov]
+    serr = np.abs(out_gpu[:, cov] - o[:, cov]) / oa[:, cov]
+    st = dict(max_rel_w=float(werr.max(initial=0)), max_scaled_v=float(serr.max(initial=0)),
+              covered=int(cov.sum()))
+    assert st["max_rel_w"] <= rtol, st
+    assert st["max_scaled_v"] <= rtol, st
+    return st

@@ -365,3 +365,100 @@ def test_cell_sharded_plans_assemble_to_full_map(engine, monkeypatch):
         W[j0:j1] = np.asarray(ww).reshape(j1 - j0, w.nx)
     o, Wo, _ = oracle_grid(w, lon, lat, vals)
     compare(out.reshape(5, -1), W.reshape(-1), o, Wo)
+
+
+@pytest.mark.parametrize("engine", ["simt", "tc_otf", "tc_pw"])
+def test_nonfinite_values_propagate_within_support(engine, monkeypatch):
+    """NaN / +-Inf sample values (reading R15, nonfinite.cuh): Eq. 1's sum makes exactly the
+    cells within R of such a sample NaN / +-Inf, as in the fp64 oracle; every other cell keeps
+    the parity rule (no 0 * NaN leak through a block's zero weights).  Channel 7 is NaN at
+    every sample, which overflows the per-launch record buffer and takes the scan path."""
+    engine = engine_env(engine, monkeypatch)
+    w = small_workload("cfg2", n=220 * 180, tracks=220, per_track=180, nx=70, ny=61,
+                       field_lon=1.2, field_lat=1.1, channels=133)
+    lon, lat, vals = make_inputs(w)
+    v = vals.numpy().copy()
+    rng = np.random.default_rng(5)
+    pick = rng.choice(w.n, 40, replace=False)
+    v[0, pick[:3]] = np.nan
+    v[5, pick[3:8]] = np.inf
+    v[5, pick[8:13]] = -np.inf
+    v[130, pick[13:40]] = np.nan
+    v[131, pick[3]] = np.inf                  # channel in the second 128-channel block
+    v[7, :] = np.nan
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, engine=engine) as p:
+        out, W = p.grid(v)
+    out = np.asarray(out, np.float64).reshape(133, -1)
+    o, Wo, _ = oracle.grid(lon.numpy(), lat.numpy(), v, w.map, w.fwhm_deg, w.support)
+    cov = Wo > 0
+    fin = np.isfinite(o)
+    assert (~fin[:, cov]).sum() > 100
+    # non-finite cells: identical class (NaN, +Inf, -Inf)
+    np.testing.assert_array_equal(np.isnan(out), np.isnan(o))
+    np.testing.assert_array_equal(np.isposinf(out), np.isposinf(o))
+    np.testing.assert_array_equal(np.isneginf(out), np.isneginf(o))
+    ok = fin & cov[None, :]
+    assert np.max(np.abs(out[ok] - o[ok]) / np.abs(o[ok])) <= 1e-5
+    np.testing.assert_allclose(np.asarray(W).reshape(-1), Wo, rtol=1e-5)
+
+
+def test_weight_image_cap_and_opt_out():
+    """hegrid_opts.weight_image_max_bytes: < 0 never builds the precomputed weight image, a
+    cap below its size leaves it unbuilt (weights computed per launch), the default builds
+    it; the maps are bit-identical either way (same weights, same accumulation order)."""
+    w = small_workload("cfg2", n=150 * 110, tracks=150, per_track=110, nx=38, ny=35,
+                       field_lon=0.7, field_lat=0.65, channels=260)
+    lon, lat, vals = make_inputs(w)
+    d = vals.cuda()
+    res = {}
+    for cap in (0, -1, 1024):
+        with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, engine="tc",
+                  weight_image_max_bytes=cap) as p:
+            out, W = p.grid(d)
+            res[cap] = (out.cpu().numpy(), W.cpu().numpy(), p.info()["weight_image_bytes"])
+    assert res[0][2] > 0 and res[-1][2] == 0 and res[1024][2] == 0
+    for cap in (-1, 1024):
+        np.testing.assert_array_equal(res[cap][0], res[0][0])
+        np.testing.assert_array_equal(res[cap][1], res[0][1])
+
+
+def test_user_layout_calls_on_two_streams_concurrently():
+    """USER_CN device calls on two streams of one plan: each takes its own scratch from the
+    plan's stream-ordered pool, so neither corrupts the other."""
+    w = small_workload("cfg2", n=120 * 100, tracks=120, per_track=100, nx=40, ny=37,
+                       field_lon=0.7, field_lat=0.6, channels=600)
+    lon, lat, vals = make_inputs(w)
+    a = vals.cuda()
+    b = (vals * 2.0 + 1.0).cuda()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg) as p:
+        ref_a, _ = p.grid(a)
+        ref_b, _ = p.grid(b)
+        torch.cuda.synchronize()
+        for _ in range(3):
+            oa, _ = p.grid(a, stream=s1)
+            ob, _ = p.grid(b, stream=s2)
+            torch.cuda.synchronize()
+            assert torch.equal(oa, ref_a) and torch.equal(ob, ref_b)
+
+
+def test_pipeline_trace_stages_are_ordered():
+    """hegrid_pipeline_trace after a profiled host call: one row per channel block, stages in
+    order (H2D, permute + accumulate, D2H) on the block's stream, blocks of one slot
+    serialised, slots used round-robin."""
+    w = small_workload("cfg2", n=120 * 100, tracks=120, per_track=100, nx=40, ny=37,
+                       field_lon=0.7, field_lat=0.6, channels=700)
+    lon, lat, vals = make_inputs(w)
+    with Plan(lon.numpy(), lat.numpy(), w.map, w.fwhm_deg, n_streams=3, channel_block=128) as p:
+        p.profile(True)
+        out, W = p.grid(vals.numpy())
+        tr = p.pipeline_trace()
+        p.profile(False)
+    assert tr.shape == (6, 5)
+    assert tr[:, 0].tolist() == [0, 1, 2, 0, 1, 2]
+    assert np.all(np.diff(tr[:, 1:], axis=1) >= 0)
+    for s in range(3):
+        rows = tr[tr[:, 0] == s]
+        assert np.all(rows[1:, 1] >= rows[:-1, 4])
+    o, Wo, _ = oracle_grid(w, lon, lat, vals)
+    compare(out.reshape(700, -1), W.reshape(-1), o, Wo)
