@@ -84,6 +84,27 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n\t"
         "}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
+// Wait with exponential nanosleep backoff (64 .. 512 ns): for roles whose waits are long and
+// off the critical path (the promoters wait a whole segment).  A try_wait with a suspend hint
+// wakes on every mbarrier event of the CTA, so a dozen warps parked in it keep re-issuing the
+// wait loop (measured: ~1 issue slot per cycle per SM taken from the pipeline roles).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t"
+        "}\n" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+    uint32_t ns = 64;
+    while (!mbar_test(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns < 512 ? 2 * ns : 512;
+    }
+}
 // Kept for the roles that usually run ahead (same wait; the hint already suspends).
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
     mbar_wait(bar, parity);
@@ -226,6 +247,45 @@ __device__ __forceinline__ void mma12_3xtf32(uint32_t d, uint32_t a0, uint32_t b
         "n"(2 * KS_STEP), "n"(3 * KS_STEP), "n"(kDescHiSw128), "n"(ALO), "n"(ALO + 8),
         "n"(ALO + 16), "n"(ALO + 24) : "memory");
 #undef HG_MMA12_KS
+}
+// mma12_3xtf32 with the accumulate flag of the first MMA as an operand: acc0 == 0 overwrites
+// D with the run's first product (a D block's first touch in a segment), so D needs no zeroing.
+template <int KS_STEP, int ALO = 32>
+__device__ __forceinline__ void mma12_3xtf32_acc(uint32_t d, uint32_t a0, uint32_t bh_lo, uint32_t bl_lo,
+                                                 uint32_t idesc, uint32_t acc0) {
+#define HG_MMA12A_KS(bh, bl, ah, al)                                                     \
+    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+" #ah "], " #bh ", %4, 1;\n\t"       \
+    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+" #ah "], " #bl ", %4, 1;\n\t"       \
+    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+" #al "], " #bh ", %4, 1;\n\t"
+    asm volatile(
+        "{\n\t"
+        ".reg .pred e, p;\n\t"
+        ".reg .b32 x1, x2, x3, y1, y2, y3;\n\t"
+        ".reg .b64 h0, h1, h2, h3, l0, l1, l2, l3;\n\t"
+        "add.u32 x1, %2, %5;\n\t"
+        "add.u32 x2, %2, %6;\n\t"
+        "add.u32 x3, %2, %7;\n\t"
+        "add.u32 y1, %3, %5;\n\t"
+        "add.u32 y2, %3, %6;\n\t"
+        "add.u32 y3, %3, %7;\n\t"
+        "mov.b64 h0, {%2, %8};\n\t"
+        "mov.b64 h1, {x1, %8};\n\t"
+        "mov.b64 h2, {x2, %8};\n\t"
+        "mov.b64 h3, {x3, %8};\n\t"
+        "mov.b64 l0, {%3, %8};\n\t"
+        "mov.b64 l1, {y1, %8};\n\t"
+        "mov.b64 l2, {y2, %8};\n\t"
+        "mov.b64 l3, {y3, %8};\n\t"
+        "setp.ne.b32 p, %13, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], h0, %4, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], l0, %4, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+%9], h0, %4, 1;\n\t"
+        HG_MMA12A_KS(h1, l1, 8, %10) HG_MMA12A_KS(h2, l2, 16, %11) HG_MMA12A_KS(h3, l3, 24, %12)
+        "}\n" :: "r"(d), "r"(a0), "r"(bh_lo), "r"(bl_lo), "r"(idesc), "n"(KS_STEP),
+        "n"(2 * KS_STEP), "n"(3 * KS_STEP), "n"(kDescHiSw128), "n"(ALO), "n"(ALO + 8),
+        "n"(ALO + 16), "n"(ALO + 24), "r"(acc0) : "memory");
+#undef HG_MMA12A_KS
 }
 // Up to three runs of one chunk (4 K-steps x 3 products each, 36 MMAs) behind one elect:
 // runs 1 and 2 are predicated on nr > 1, nr > 2.  Every operand base enters the asm once
