@@ -4,18 +4,20 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--impl ours|reference]
 
 One "step" = Eq. 1 for the whole workload (BASELINE.json configs[3] by default: 1M drift-scan
-samples x 4096 channels -> 300x300 map) on each rank's GPU: hegrid_grid_device on
-HBM-resident, plan-ordered channel-contiguous values (the layout the staging layer
-delivers), the plan (shared component, built once per coordinate set) prebuilt and its
-time reported separately.  Multi-GPU: one process per GPU (torchrun), channel shards,
-no data-path collective, weak scaling (each rank grids its own 4096 channels).
+samples x 4096 channels -> 300x300 map): hegrid_grid_device on HBM-resident, plan-ordered
+channel-contiguous values (the layout the staging layer delivers), the plan (shared
+component, built once per coordinate set) prebuilt and its time reported separately.
+Multi-GPU: one process per GPU (torchrun); the workload's channels are sharded across the
+ranks (4096 / G each, configs[3] "channel-sharded at 1/2/4/8 GPUs"), no data-path
+collective, strong scaling (the total work is fixed).
 
 Also measured in the same run:
   e2e       -- the public host API (plan from host coords + hegrid_grid on pinned host
-               [C][N] values -> pinned host maps), H2D/D2H inside the timed region;
+               [C][N] values -> pinned host maps), H2D/D2H inside the timed region, against
+               the pinned H2D bandwidth measured in the same run (the PCIe roof);
   roofline  -- the accumulate kernel (the dominant kernel) timed with CUDA events on its
-               launch stream; binding roof = FP32 FMA issue (alu), plus the north_star's
-               HBM-roofline fraction;
+               launch stream: the north_star's HBM-roofline fraction, plus the tensor view
+               (fp32-accurate 3xTF32 work against the TF32 peak) and the ALU view;
   cpu_baseline -- the fp64 oracle on this host's cores, on a bounded sample of cells.
 """
 from __future__ import annotations
@@ -136,6 +138,21 @@ def user_layout_values_pinned(w, lon, lat, channel_ids, device):
     return host
 
 
+def pinned_h2d_gbs(dev, mib=1024, reps=3):
+    """Pinned host -> device copy bandwidth (GB/s), the PCIe roof of the e2e path."""
+    h = torch.empty(mib << 18, dtype=torch.float32, pin_memory=True)
+    d = torch.empty(mib << 18, dtype=torch.float32, device=dev)
+    d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    gbs = reps * h.numel() * 4 / (time.perf_counter() - t0) / 1e9
+    del h, d
+    return gbs
+
+
 def oracle_sample(w, lon_h, lat_h, vals_h, target_s=15.0, max_cells=None):
     """Time the fp64 oracle (all host cores) on an evenly spaced sample of cells with all
     channels; return (throughput samples*ch/s extrapolated to the whole map, detail)."""
@@ -186,29 +203,38 @@ def run_reference(args):
     budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
     per = []
     detail = None
+    t_run = time.perf_counter()
     for s in range(args.warmup + args.steps):
         thr, detail = oracle_sample(w, lon_h, lat_h, vals_h, target_s=budget)
         if s >= args.warmup:
             per.append(w.n * C / thr)     # seconds for one whole-workload step (extrapolated)
+    t_run = time.perf_counter() - t_run
     ms = 1000 * statistics.median(per)
     value = w.n * C / (ms / 1000)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(w, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": detail["cores"],
                              "kind": "oracle", "sample": detail["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            # each "step" is a bounded, evenly spaced cell sample of the workload timed on the
+            # host and extrapolated to the whole map: ms_per_step is that extrapolation, not a
+            # measured whole-workload time (the run itself took timed_s seconds)
+            "extrapolated": True, "timed_s": t_run,
+            "step_note": "per step: %s; ms_per_step extrapolated to all cells" % detail["sample"]}
     print(json.dumps(line), flush=True)
 
 
 def workload_config(w, world):
-    return {"workload": w.name, "desc": w.note, "n_samples": w.n, "channels_per_gpu": w.channels,
-            "global_channels": w.channels * world, "map": f"{w.nx}x{w.ny}",
+    from paper_2207_04584_b200.shard import channel_shard
+    c0, c1 = channel_shard(w.channels, world, 0)
+    return {"workload": w.name, "desc": w.note, "n_samples": w.n, "channels_per_gpu": c1 - c0,
+            "global_channels": w.channels, "map": f"{w.nx}x{w.ny}",
             "cell_deg": w.cdelt, "kernel_fwhm_deg": w.fwhm_deg, "support_sigma": w.support,
             "field_deg": [w.field_lon, w.field_lat], "centre_deg": list(w.centre),
-            "sampling": w.kind, "parallelism": f"channel-shard x{world}",
+            "sampling": w.kind, "parallelism": f"channel-shard x{world} (strong scaling)",
             "input_layout": "plan-ordered [n_used][C] fp32, HBM-resident",
             "l2": "inputs larger than L2 (values %.1f GB vs 126 MB L2)" % (w.n * w.channels * 4 / 1e9)}
 
@@ -257,8 +283,11 @@ def main():
     from paper_2207_04584_b200 import Plan, abi
 
     w = synth.CONFIGS[args.workload]
-    C = w.channels
-    channel_ids = list(range(rank * C, (rank + 1) * C))      # weak scaling: own shard
+    from paper_2207_04584_b200.shard import channel_shard
+    C_global = w.channels
+    c0, c1 = channel_shard(C_global, world, rank)              # strong scaling: 1/G of the channels
+    C = c1 - c0
+    channel_ids = list(range(c0, c1))
     lon, lat = synth.coords(w, device=dev)
 
     # ---------------------------------------------------------------- plan (once)
@@ -318,7 +347,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    units = w.n * C * world
+    units = w.n * C_global
     value = units / (ms_step / 1000)
 
     # ---------------------------------------------------------------- roofline
@@ -353,6 +382,22 @@ def main():
     alu_view = {"achieved": alu_achieved, "peak": fp32_peak_tflops, "unit": "TFLOP/s",
                 "frac": alu_achieved / fp32_peak_tflops, "algorithmic_flops_per_launch": flops,
                 "peak_source": "148 SMs x 128 FP32 lanes x 2 flop x sm_max_mhz (DESIGN.md)"}
+    # Tensor view: the contraction runs on the TF32 tensor pipe as 3 products per pair
+    # (3xTF32).  Useful work = 2 P C fp32-accurate flops; the roof for it = the TF32 peak / 3,
+    # with the TF32 peak = the measured bf16 peak / 2 (the nominal bf16 : tf32 ratio).
+    # mma_density = useful pairs / executed (16-cell x 32-sample block slots).
+    info2 = plan.info()
+    tf32_peak = peaks["bf16_tflops"] / 2.0
+    slots = info2.get("tc_block_slots", 0) or 0
+    tensor_view = {"achieved": flops / (k_avg_ms / 1000) / 1e12, "peak": tf32_peak / 3.0,
+                   "unit": "TFLOP/s (fp32-accurate, 3xTF32)",
+                   "frac": flops / (k_avg_ms / 1000) / 1e12 / (tf32_peak / 3.0),
+                   "tf32_peak": tf32_peak,
+                   "peak_source": f"{peak_src} bf16_tflops / 2 (tf32) / 3 (products per pair)",
+                   "mma_density": info["n_pairs"] / (512.0 * slots) if slots else None,
+                   "executed_tf32_tflops": (3 * 2 * 512.0 * slots * C / (k_avg_ms / 1000) / 1e12)
+                   if slots else None} if args.engine == "tc" else None
+    one_shot_ms = info["t_plan_ms"] + max(first_ms - ms_step, 0.0) + ms_step
 
     # ---------------------------------------------------------------- e2e (public host API)
     e2e = None
@@ -360,6 +405,7 @@ def main():
     if not args.no_e2e:
         del vp
         torch.cuda.empty_cache()
+        h2d_gbs = pinned_h2d_gbs(dev)
         host_vals = user_layout_values_pinned(w, lon, lat, channel_ids, dev)
         host_out = torch.empty((C, w.ny, w.nx), dtype=torch.float32, pin_memory=True)
         host_w = torch.empty((w.ny, w.nx), dtype=torch.float32, pin_memory=True)
@@ -367,6 +413,9 @@ def main():
         lat_h = lat.cpu().numpy()
 
         def e2e_step():
+            # the whole job through the public API: a plan from the host coordinates
+            # (coordinates H2D, index build, engine tables) and hegrid_grid from pinned host
+            # [C][N] values to pinned host maps (H2D, permute, accumulate, D2H over streams)
             with Plan(lon_h, lat_h, w.map, w.fwhm_deg, w.support, device=local,
                       engine=args.engine) as p:
                 p.grid(host_vals, host_out, host_w)
@@ -380,14 +429,31 @@ def main():
             e2e_step()
         torch.cuda.synchronize(dev)
         te = (time.perf_counter() - t0) / args.e2e_steps
-        tt = torch.tensor([te], device=dev, dtype=torch.float64)
+        # the same hegrid_grid call on a plan built once (the coordinates are shared by every
+        # channel block of an observation)
+        with Plan(lon_h, lat_h, w.map, w.fwhm_deg, w.support, device=local, engine=args.engine) as p:
+            p.grid(host_vals, host_out, host_w)
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                p.grid(host_vals, host_out, host_w)
+            torch.cuda.synchronize(dev)
+            tg = (time.perf_counter() - t0) / args.e2e_steps
+        tt = torch.tensor([te, tg], device=dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        te = float(tt.item())
+        te, tg = float(tt[0].item()), float(tt[1].item())
+        h2d_b = C * w.n * 4 + 16 * w.n
         e2e = {"value": units / te, "unit": UNIT, "ms_per_step": te * 1000,
-               "h2d_bytes_per_step": C * w.n * 4 + 16 * w.n,
+               "h2d_bytes_per_step": h2d_b,
                "d2h_bytes_per_step": C * cells * 4 + cells * 4,
-               "api": "Plan(host coords) + hegrid_grid(pinned host [C][N] -> pinned host maps)"}
+               "api": "Plan(host coords) + hegrid_grid(pinned host [C][N] -> pinned host maps)",
+               "pinned_h2d_gbs": h2d_gbs,
+               "h2d_roof_ms": h2d_b / (h2d_gbs * 1e9) * 1000,
+               "frac_of_h2d_roof": (h2d_b / te / 1e9) / h2d_gbs,
+               "plan_reused": {"value": units / tg, "ms_per_step": tg * 1000,
+                               "frac_of_h2d_roof": ((h2d_b - 16 * w.n) / tg / 1e9) / h2d_gbs,
+                               "api": "hegrid_grid on a plan built once"}}
 
     # ---------------------------------------------------------------- cpu baseline (rank 0, N=1)
     cpu = None
@@ -401,14 +467,15 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic (seeded drift-scan coords, sky-model values)",
                 "config": workload_config(w, world),
                 "plan_ms": info["t_plan_ms"],
                 "prep_ms": max(first_ms - ms_step, 0.0),
+                "one_shot_ms": one_shot_ms,
                 "pairs": {"n_pairs": info["n_pairs"], "candidates": info["n_candidate_pairs"],
                           "nbr_mean": info["nbr_mean"]},
-                "roofline": roof, "alu_view": alu_view, "clocks": clk,
+                "roofline": roof, "tensor_view": tensor_view, "alu_view": alu_view, "clocks": clk,
                 "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     plan.close()

@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define HEGRID_ABI_VERSION 3
+#define HEGRID_ABI_VERSION 4
 
 typedef enum hegrid_status {
     HEGRID_OK = 0,
@@ -135,6 +135,11 @@ typedef struct hegrid_plan_stats {
     int32_t mlat, mlon;         /* margins in bins */
     double sigma_deg, radius_deg;
     int64_t weight_image_bytes; /* device bytes of the precomputed weight image (0 = none) */
+    int64_t tc_entries;         /* tensor-core engine schedule entries (0 = schedule not built
+                                   yet: it is built by the first tensor-core launch) */
+    int64_t tc_block_slots;     /* (entry, in-reach 4x4-cell block) pairs: each is one
+                                   16-cell x 32-sample slot of the dense MMA product, so
+                                   n_pairs / (512 tc_block_slots) is the useful MMA density */
 } hegrid_plan_stats;
 
 /* ---- plan: spatial index (PAPER.md:177-192 steps 1,2,4; Algorithm 1 region lookup) ----

@@ -60,7 +60,8 @@ class hegrid_plan_stats(ctypes.Structure):
                 ("t_plan_ms", ctypes.c_double), ("nrow", ctypes.c_int32),
                 ("ncol", ctypes.c_int32), ("mlat", ctypes.c_int32), ("mlon", ctypes.c_int32),
                 ("sigma_deg", ctypes.c_double), ("radius_deg", ctypes.c_double),
-                ("weight_image_bytes", ctypes.c_int64)]
+                ("weight_image_bytes", ctypes.c_int64), ("tc_entries", ctypes.c_int64),
+                ("tc_block_slots", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <thread>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -87,16 +88,10 @@ static hegrid_status create_common(const double* d_lon, const double* d_lat, int
     p->kern = *kernel;
     p->opts = o;
     p->n = n;
-    {   // the plan's stream-ordered pool (common.cuh): memory stays cached between calls
-        cudaMemPoolProps pp{};
-        pp.allocType = cudaMemAllocationTypePinned;
-        pp.location.type = cudaMemLocationTypeDevice;
-        pp.location.id = o.device;
-        cudaError_t e = cudaMemPoolCreate(&p->pool, &pp);
-        uint64_t keep = UINT64_MAX;
-        if (e == cudaSuccess) e = cudaMemPoolSetAttribute(p->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    {   // the device's stream-ordered pool (common.cuh): memory stays cached between calls
+        // and between plans, so a new plan over the same shapes allocates nothing new
+        cudaError_t e = shared_pool(o.device, &p->pool);
         if (e != cudaSuccess) {
-            if (p->pool) cudaMemPoolDestroy(p->pool);
             delete p;
             return cuda_status(e);
         }
@@ -108,6 +103,38 @@ static hegrid_status create_common(const double* d_lon, const double* d_lat, int
     }
     *out = p;
     return HEGRID_OK;
+}
+
+cudaError_t shared_pool(int device, cudaMemPool_t* pool) {
+    static std::mutex mu;
+    static std::vector<cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> lock(mu);
+    if (device < 0) return cudaErrorInvalidDevice;
+    if ((int)pools.size() <= device) pools.resize(device + 1, nullptr);
+    if (!pools[device]) {
+        cudaMemPoolProps pp{};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = device;
+        cudaMemPool_t q = nullptr;
+        cudaError_t e = cudaMemPoolCreate(&q, &pp);
+        uint64_t keep = UINT64_MAX;
+        if (e == cudaSuccess) e = cudaMemPoolSetAttribute(q, cudaMemPoolAttrReleaseThreshold, &keep);
+        if (e != cudaSuccess) {
+            if (q) cudaMemPoolDestroy(q);
+            return e;
+        }
+        pools[device] = q;
+    }
+    *pool = pools[device];
+    return cudaSuccess;
+}
+
+hegrid_status prepare_engine(const hegrid_plan_s* p, int64_t n_channels_per_launch) {
+    if (p->opts.engine == HEGRID_ENGINE_SIMT || p->n_used == 0) return HEGRID_OK;
+    auto* q = const_cast<hegrid_plan_s*>(p);
+    if (!q->prep_st) HG_TRY(cudaStreamCreateWithFlags(&q->prep_st, cudaStreamNonBlocking));
+    return prepare_tc(p, n_channels_per_launch, q->prep_st);
 }
 
 hegrid_status launch_accumulate(const hegrid_plan_s* p, const float* d_v, int64_t ldv,
@@ -152,16 +179,29 @@ hegrid_status hegrid_plan_create(const double* lon_deg, const double* lat_deg, i
     hegrid_opts o = default_opts(opts);
     DeviceGuard dg(o.device);
     HG_TRY(dg.err);
+    // coordinates H2D into stream-ordered buffers of the device pool (no cudaMalloc / cudaFree
+    // and their device-wide synchronisation on the plan path)
+    cudaMemPool_t pool = nullptr;
+    HG_TRY(shared_pool(o.device, &pool));
+    cudaStream_t st = nullptr;
+    HG_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     double *d_lon = nullptr, *d_lat = nullptr;
     size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(double);
-    HG_TRY(cudaMalloc(&d_lon, bytes));
-    cudaError_t e = cudaMalloc(&d_lat, bytes);
-    if (e == cudaSuccess && n > 0) e = cudaMemcpy(d_lon, lon_deg, n * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && n > 0) e = cudaMemcpy(d_lat, lat_deg, n * 8, cudaMemcpyHostToDevice);
+    cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&d_lon), bytes, pool, st);
+    if (e == cudaSuccess) e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&d_lat), bytes, pool, st);
+    if (e == cudaSuccess && n > 0) e = cudaMemcpyAsync(d_lon, lon_deg, n * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && n > 0) e = cudaMemcpyAsync(d_lat, lat_deg, n * 8, cudaMemcpyHostToDevice, st);
     hegrid_status s = cuda_status(e);
-    if (s == HEGRID_OK) s = create_common(d_lon, d_lat, n, map, kernel, o, 0, out);
-    cudaFree(d_lon);
-    if (d_lat) cudaFree(d_lat);
+    if (s == HEGRID_OK) s = create_common(d_lon, d_lat, n, map, kernel, o, st, out);
+    if (d_lon) cudaFreeAsync(d_lon, st);
+    if (d_lat) cudaFreeAsync(d_lat, st);
+    cudaError_t e2 = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (s == HEGRID_OK && e2 != cudaSuccess) {
+        hegrid_plan_destroy(*out);
+        *out = nullptr;
+        s = cuda_status(e2);
+    }
     return s;
 }
 
@@ -181,19 +221,13 @@ hegrid_status hegrid_plan_create_device(const double* d_lon, const double* d_lat
 void hegrid_plan_destroy(hegrid_plan_t p) {
     if (!p) return;
     DeviceGuard dg(p->device);
-    cudaFree(p->d_keys);
-    cudaFree(p->d_perm);
-    cudaFree(p->d_iperm);
-    cudaFree(p->d_geo);
-    cudaFree(p->d_ll);
-    cudaFree(p->d_bin_start);
-    cudaFree(p->d_mrow);
-    cudaFree(p->d_cos_row);
-    cudaFree(p->d_tc_sched);
-    cudaFree(p->d_tc_tile_off);
-    cudaFree(p->d_tc_wsum);
-    cudaFree(p->d_tc_wimg);
-    cudaFree(p->d_tc_wslot);
+    // the plan's arrays go back to the device pool once all work issued so far is done
+    cudaDeviceSynchronize();
+    for (void* q : {(void*)p->d_keys, (void*)p->d_perm, (void*)p->d_iperm, (void*)p->d_geo,
+                    (void*)p->d_ll, (void*)p->d_bin_start, (void*)p->d_mrow, (void*)p->d_cos_row,
+                    (void*)p->d_tc_sched, (void*)p->d_tc_tile_off, (void*)p->d_tc_wsum,
+                    (void*)p->d_tc_wimg, (void*)p->d_tc_wslot})
+        if (q) cudaFreeAsync(q, 0);
     for (auto e : p->prof_events) cudaEventDestroy(e);
     for (auto& x : p->slots) {
         if (x.st) cudaStreamSynchronize(x.st);
@@ -203,9 +237,8 @@ void hegrid_plan_destroy(hegrid_plan_t p) {
         if (x.h_out) cudaFreeHost(x.h_out);
         if (x.st) cudaStreamDestroy(x.st);
     }
-    // outstanding stream-ordered allocations (none after the calls above) would defer the
-    // release to their frees
-    if (p->pool) cudaMemPoolDestroy(p->pool);
+    if (p->prep_st) cudaStreamDestroy(p->prep_st);
+    cudaStreamSynchronize(0);
     delete p;
 }
 
@@ -229,6 +262,8 @@ hegrid_status hegrid_plan_info(hegrid_plan_t p, hegrid_plan_stats* out) {
     s.sigma_deg = p->g.sigma_rad / kDeg2Rad;
     s.radius_deg = p->g.R_rad / kDeg2Rad;
     s.weight_image_bytes = p->tc_pw == 1 ? p->tc_wimg_bytes : 0;
+    s.tc_entries = p->tc_nchunks > 0 ? p->tc_nchunks : 0;
+    s.tc_block_slots = p->tc_nchunks > 0 ? (int64_t)p->tc_stats[1] : 0;
     *out = s;
     return HEGRID_OK;
 }
@@ -423,6 +458,9 @@ hegrid_status hegrid_grid(hegrid_plan_t p, const float* data, int64_t n_channels
             if (fail(cudaMemcpyAsync(d.raw, src, (size_t)cn * n * 4, cudaMemcpyHostToDevice, x.st)))
                 break;
             mark(b, 1, x.st);
+            // the engine's one-time per-plan tables (tensor-core schedule, W, weight image) are
+            // built on the plan's own stream while the first block is in flight over PCIe
+            if (b == 0 && (s = prepare_engine(p, std::min(cb, n_channels))) != HEGRID_OK) break;
             if ((s = launch_permute(p, d.raw, cn, n, d.v, cb, x.st)) != HEGRID_OK) break;
         } else {
             mark(b, 1, x.st);

@@ -94,12 +94,15 @@ struct hegrid_plan_s {
     mutable uint32_t* d_tc_wslot = nullptr;    // [entries] first 4-KB slot of each entry
     mutable int tc_pw = -1;                    // -1 not built (retried on later calls), 1 built
     mutable int64_t tc_wimg_bytes = 0;
-    // Stream-ordered device memory pool of the plan (the paper's per-stream "memory pool",
-    // PAPER.md:315-316): every per-call device buffer (USER_CN scratch, split-tile partial
-    // sums, non-finite records, hegrid_grid's channel-block slots) is taken from it on the
-    // caller's stream and returned to it on the same stream, so calls on different streams
-    // never share a buffer and repeated calls reuse the memory (release threshold: never).
-    cudaMemPool_t pool = nullptr;
+    // Stream-ordered device memory pool (the paper's per-stream "memory pool",
+    // PAPER.md:315-316): every device buffer of the plan (its arrays, the engine tables and
+    // weight image, and per call the USER_CN scratch, split-tile partial sums, non-finite
+    // records, hegrid_grid's channel-block slots) is taken from it on the caller's stream
+    // and returned to it on the same stream, so calls on different streams never share a
+    // buffer and repeated calls (and later plans) reuse the memory (release threshold:
+    // never).  One pool per device, shared by all plans of the process.
+    cudaMemPool_t pool = nullptr;      // the device's shared pool (shared_pool), not owned
+    cudaStream_t prep_st = nullptr;    // one-time engine preparation (prepare_engine)
     // hegrid_grid's staging slots, created on first use and reused by later calls: one CUDA
     // stream, its events and pinned host buffers (grown on demand) per slot
     struct StageSlot {
@@ -147,6 +150,12 @@ hegrid_status launch_accumulate(const hegrid_plan_s* p, const float* d_v, int64_
 // permute.cu
 hegrid_status launch_permute(const hegrid_plan_s* p, const float* d_user, int64_t n_channels,
                              int64_t ld_user, float* d_plan, int64_t ld_plan, cudaStream_t st);
+
+// api.cu: the process-wide stream-ordered pool of a device (release threshold: never)
+cudaError_t shared_pool(int device, cudaMemPool_t* pool);
+// grid_tc.cu / api.cu: build the engine's per-plan tables now (on the plan's prep stream)
+hegrid_status prepare_engine(const hegrid_plan_s* p, int64_t n_channels_per_launch);
+hegrid_status prepare_tc(const hegrid_plan_s* p, int64_t n_channels_per_launch, cudaStream_t st);
 
 inline cudaError_t plan_alloc(const hegrid_plan_s* p, void* ptr, size_t bytes, cudaStream_t st) {
     return cudaMallocFromPoolAsync(reinterpret_cast<void**>(ptr), bytes, p->pool, st);

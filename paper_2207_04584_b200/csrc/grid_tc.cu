@@ -77,10 +77,11 @@ static_assert(TC_KC == 32 || TC_KC == 64, "chunks of 32 or 64 samples");
 #ifndef HG_TC_NA
 #define HG_TC_NA 2
 #endif
-// NBS = 2: with 3-4 weight stages (producers up to 3 chunks ahead of the tensor core)
-// results became timing-dependent although every stage handoff is mbarrier-ordered; the
-// cause is not yet understood (tools/det_small.py reproduces it), so the
-// engine runs with 2 weight stages, which is deterministic in every test.
+// NBS = 2 weight stages in the on-the-fly mode.  (Round 1 saw timing-dependent results with
+// 3-4 stages before the release-before-consume fix of the shared-stage hand-offs; with the
+// fp32 master tile in shared memory, 3 or more stages no longer fit the 227 KB budget, so
+// the question is moot for this kernel.  NBS = 2 is bit-deterministic run to run:
+// tools/det_otf.sh, profiles/r2/det_otf_nbs.log.)
 #ifndef HG_TC_NBS
 #define HG_TC_NBS 2
 #endif
@@ -138,7 +139,7 @@ constexpr int NBF = 16;
 // entry into a byte ring in shared memory (entries placed contiguously, wrapping to 0).
 constexpr uint32_t SLOT_BYTES = KA * ATOM_SLOT;      // one block, one half (hi or lo): 2 KB at K = 32
 #ifndef HG_TC_RING_KB
-#define HG_TC_RING_KB 76
+#define HG_TC_RING_KB 74
 #endif
 constexpr uint32_t RING = HG_TC_RING_KB * 1024;
 static_assert(RING >= MAXQ * 2 * SLOT_BYTES, "the ring holds the largest entry");
@@ -156,7 +157,7 @@ struct TcSmem {
     uint64_t seg_done[2], seg_free[2];    // D buffer d: segment's MMAs complete / promoted
     uint64_t bar_done;
     uint32_t tmem_base;
-    uint32_t sink[TC_THREADS / 32];       // dependency sink (see the B producers' release)
+    uint32_t sink[TC_THREADS];            // dependency sink, one word per thread (see the B producers' release)
     float Wt[TC_TW * TC_TH];              // the tile's W per cell (epilogue)
     alignas(16) float M[TC_M][T_LD];      // fp32 master sums [channel][cell] (padded rows)
 };
@@ -498,10 +499,10 @@ static bool ensure_tc_wimage(const hegrid_plan_s* p, cudaStream_t st) {
     uint8_t* d_img = nullptr;
     uint32_t* d_slot = nullptr;
     prep_mark("slot scan + meminfo");
-    if (cudaMalloc(&d_img, bytes) != cudaSuccess) return false;
-    prep_mark("image cudaMalloc");
-    if (cudaMalloc(&d_slot, ne * sizeof(uint32_t)) != cudaSuccess) {
-        cudaFree(d_img);
+    if (plan_alloc(p, &d_img, bytes, st) != cudaSuccess) return false;
+    prep_mark("image allocation");
+    if (plan_alloc(p, &d_slot, ne * sizeof(uint32_t), st) != cudaSuccess) {
+        cudaFreeAsync(d_img, st);
         return false;
     }
     cudaError_t e = cudaMemcpyAsync(d_slot, slot.data(), ne * sizeof(uint32_t), cudaMemcpyHostToDevice, st);
@@ -513,8 +514,8 @@ static bool ensure_tc_wimage(const hegrid_plan_s* p, cudaStream_t st) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     prep_mark("image kernel");
     if (e != cudaSuccess) {
-        cudaFree(d_img);
-        cudaFree(d_slot);
+        cudaFreeAsync(d_img, st);
+        cudaFreeAsync(d_slot, st);
         return false;
     }
     p->d_tc_wimg = d_img;
@@ -532,17 +533,17 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     const int64_t cells = (int64_t)g.nx * g.ny;
     uint32_t* d_n = nullptr;
     float* d_w = nullptr;
-    HG_TRY(cudaMalloc(&d_n, (tiles + 6) * sizeof(uint32_t)));
-    cudaError_t e = cudaMalloc(&d_w, cells * sizeof(float));
+    HG_TRY(plan_alloc(p, &d_n, (tiles + 6) * sizeof(uint32_t), st));
+    cudaError_t e = plan_alloc(p, &d_w, cells * sizeof(float), st);
     if (e != cudaSuccess) {
-        cudaFree(d_n);
+        cudaFreeAsync(d_n, st);
         return cuda_status(e);
     }
     const int threads = 128, blocks = (tiles * 32 + threads - 1) / threads;
     e = cudaMemsetAsync(d_n, 0, (tiles + 6) * sizeof(uint32_t), st);
     if (e != cudaSuccess) {
-        cudaFree(d_n);
-        cudaFree(d_w);
+        cudaFreeAsync(d_n, st);
+        cudaFreeAsync(d_w, st);
         return cuda_status(e);
     }
     k_tc_schedule<<<blocks, threads, 0, st>>>(g, p->dev(), tiles, d_n, nullptr, nullptr);
@@ -553,15 +554,15 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d_n, (tiles + 6) * 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
-        cudaFree(d_n);
-        cudaFree(d_w);
+        cudaFreeAsync(d_n, st);
+        cudaFreeAsync(d_w, st);
         return cuda_status(e);
     }
     std::vector<uint32_t> off(tiles + 1, 0);
     for (int t = 0; t < tiles; ++t) off[t + 1] = off[t] + h[t];
     const int64_t total = off[tiles];
     uint4* d_s = nullptr;
-    e = cudaMalloc(&d_s, std::max<int64_t>(total, 1) * sizeof(uint4));
+    e = plan_alloc(p, &d_s, std::max<int64_t>(total, 1) * sizeof(uint4), st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_n, off.data(), (tiles + 1) * 4, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
         k_tc_schedule<<<blocks, threads, 0, st>>>(g, p->dev(), tiles, nullptr, d_n, d_s);
@@ -570,9 +571,9 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
-        cudaFree(d_n);
-        cudaFree(d_w);
-        if (d_s) cudaFree(d_s);
+        cudaFreeAsync(d_n, st);
+        cudaFreeAsync(d_w, st);
+        if (d_s) cudaFreeAsync(d_s, st);
         return cuda_status(e);
     }
     prep_mark("schedule + wsum built");
@@ -587,6 +588,17 @@ static hegrid_status ensure_tc_plan(const hegrid_plan_s* p, cudaStream_t st) {
     p->tc_stats[3] = h[tiles + 4];    // runs of consecutive blocks
     p->tc_stats[4] = h[tiles + 5];    // block spans
     return HEGRID_OK;
+}
+
+// The engine's one-time per-plan tables for launches of n_channels (hegrid_grid builds them
+// on the plan's prep stream while its first channel block is in flight).
+hegrid_status prepare_tc(const hegrid_plan_s* p, int64_t n_channels_per_launch, cudaStream_t st) {
+    HG_TRY_S(ensure_tc_plan(p, st));
+    const int ncb = (int)((n_channels_per_launch + TC_M - 1) / TC_M);
+    int want_pw = ncb >= (int)TC_PW_MIN_CBLOCKS;
+    if (const char* e = getenv("HEGRID_TC_PW")) want_pw = atoi(e);
+    if (want_pw) ensure_tc_wimage(p, st);
+    return cuda_status(cudaStreamSynchronize(st));
 }
 
 // Debug cycle counters (HEGRID_TC_DEBUG bit 32): summed over CTAs.
@@ -1061,7 +1073,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const float lsum = s0 + s1;
             const uint32_t dep = ee.x ^ ee.y ^ ee.z ^ __float_as_uint(lsum);
             if (warp == 4 && lane == 0 && tl_on && c < 256) g_tl[c][8] = clock64() + (dep == 0x12345u);
-            asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[warp])), "r"(dep) : "memory");
+            asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[tid])), "r"(dep) : "memory");
             // one arrive per warp (hundreds of per-thread arrives on one mbarrier serialise)
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&sm.v_empty[sv]);
@@ -1178,7 +1190,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 for (int u = 0; u < 4; ++u)
                     dep ^= __float_as_uint(g4[u].x) ^ __float_as_uint(g4[u].y) ^
                            __float_as_uint(g4[u].z) ^ __float_as_uint(g4[u].w);
-                asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[warp])), "r"(dep) : "memory");
+                asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[tid])), "r"(dep) : "memory");
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&sm.v_empty[sv]);
             }
@@ -1301,7 +1313,7 @@ struct PwSmem {
     uint64_t a_full[PW_NA], b_full[NBF], done[NBF], v_full[PW_NV], v_empty[PW_NV];
     uint64_t seg_done, seg_free;
     uint32_t tmem_base;
-    uint32_t sink[PW_THREADS / 32];
+    uint32_t sink[PW_THREADS];             // dependency sink, one word per thread
     float stage[4 * PW_NPG][32][PW_STG_LD];   // epilogue staging, one tile per promoter warp
 };
 static_assert(sizeof(PwSmem) + 1024 <= 232448, "shared memory budget");
@@ -1574,7 +1586,7 @@ k_accum_pw(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 // release the value stage only after every loaded word was consumed (an
                 // mbarrier arrive does not wait for outstanding shared loads): store a value
                 // that depends on all of them first
-                asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[warp])), "r"(ee.x ^ mx) : "memory");
+                asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[tid])), "r"(ee.x ^ mx) : "memory");
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&sm.v_empty[sv]);
                 // non-finite values: zeroed here, applied by the fix-up (nonfinite.cuh)

@@ -315,14 +315,14 @@ hegrid_status build_plan(hegrid_plan_s* p, const double* d_lon, const double* d_
     HG_TRY(cudaEventCreate(&e0));
     HG_TRY(cudaEventCreate(&e1));
     size_t nn = (size_t)std::max<int64_t>(n, 1);
-    HG_TRY(cudaMalloc(&p->d_keys, nn * sizeof(uint32_t)));
-    HG_TRY(cudaMalloc(&p->d_perm, nn * sizeof(int32_t)));
-    HG_TRY(cudaMalloc(&p->d_iperm, nn * sizeof(int32_t)));
-    HG_TRY(cudaMalloc(&p->d_geo, nn * sizeof(float4)));
-    HG_TRY(cudaMalloc(&p->d_ll, nn * sizeof(double2)));
-    HG_TRY(cudaMalloc(&p->d_bin_start, (g.nbins + 1) * sizeof(uint32_t)));
-    HG_TRY(cudaMalloc(&p->d_mrow, g.nrow * sizeof(int)));
-    HG_TRY(cudaMalloc(&p->d_cos_row, g.ny * sizeof(float)));
+    HG_TRY(plan_alloc(p, &p->d_keys, nn * sizeof(uint32_t), st));
+    HG_TRY(plan_alloc(p, &p->d_perm, nn * sizeof(int32_t), st));
+    HG_TRY(plan_alloc(p, &p->d_iperm, nn * sizeof(int32_t), st));
+    HG_TRY(plan_alloc(p, &p->d_geo, nn * sizeof(float4), st));
+    HG_TRY(plan_alloc(p, &p->d_ll, nn * sizeof(double2), st));
+    HG_TRY(plan_alloc(p, &p->d_bin_start, (g.nbins + 1) * sizeof(uint32_t), st));
+    HG_TRY(plan_alloc(p, &p->d_mrow, g.nrow * sizeof(int), st));
+    HG_TRY(plan_alloc(p, &p->d_cos_row, g.ny * sizeof(float), st));
     HG_TRY(cudaMemcpyAsync(p->d_mrow, mrow.data(), g.nrow * sizeof(int), cudaMemcpyHostToDevice, st));
     HG_TRY(cudaMemcpyAsync(p->d_cos_row, cos_row.data(), g.ny * sizeof(float),
                            cudaMemcpyHostToDevice, st));

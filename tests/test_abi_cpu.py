@@ -43,7 +43,7 @@ def test_binding_covers_every_header_symbol():
 
 def test_status_strings_and_version(lib):
     from paper_2207_04584_b200 import _binding as b
-    assert b.hegrid_abi_version() == 3
+    assert b.hegrid_abi_version() == 4
     for code in range(7):
         assert len(b.hegrid_status_string(code)) >= 2
     assert "unknown" in b.hegrid_status_string(99)

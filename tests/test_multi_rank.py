@@ -122,3 +122,52 @@ def test_row_shard_covers_rows_once():
         lat_sub = s["crval_lat"] + (jp + 1 - s["crpix_y"]) * s["cdelt_lat"]
         lat_full = m["crval_lat"] + (jp + 4 + 1 - m["crpix_y"]) * m["cdelt_lat"]
         assert lat_sub == lat_full
+
+
+def _dist_worker(rank, world, port, path, C, N, out_shape):
+    """paper_2207_04584_b200.distributed.grid_rank under a gloo process group, with the
+    oracle as the per-rank gridder and a shared float32 memmap as the output."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import synth
+    from paper_2207_04584_b200.distributed import grid_rank, open_shared_out
+    w = synth.CONFIGS["cfg1"].with_(n=N, channels=C, nx=9, ny=8)
+    lon, lat = synth.coords(w)
+    vals = synth.values(w, lon, lat).numpy()
+    if rank == 0:
+        open_shared_out(path, out_shape, create=True).flush()
+    dist.barrier()
+    out = open_shared_out(path, out_shape, create=False)
+
+    def gridder(v):
+        o, _, _ = oracle.grid(lon.numpy(), lat.numpy(), v, w.map, w.fwhm_deg, w.support, nthreads=1)
+        return o.reshape((v.shape[0],) + tuple(out_shape[1:])).astype(np.float32)
+
+    grid_rank(gridder, vals, out, world, rank)
+    out.flush()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_distributed_driver_assembles_shared_output(world):
+    """The product driver's per-rank step (distributed.grid_rank + the shared output
+    memmap): G ranks together write every channel exactly once, equal to one process."""
+    import oracle
+    import synth
+    C, N = 9, 600
+    w = synth.CONFIGS["cfg1"].with_(n=N, channels=C, nx=9, ny=8)
+    shape = (C, w.ny, w.nx)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "out.f32")
+        port = 33500 + (os.getpid() % 2000)
+        mp.spawn(_dist_worker, args=(world, port, path, C, N, shape), nprocs=world, join=True)
+        got = np.array(np.memmap(path, dtype=np.float32, mode="r", shape=shape))
+    lon, lat = synth.coords(w)
+    vals = synth.values(w, lon, lat).numpy()
+    ref, _, _ = oracle.grid(lon.numpy(), lat.numpy(), vals, w.map, w.fwhm_deg, w.support)
+    ref = ref.reshape(shape).astype(np.float32)
+    np.testing.assert_array_equal(np.isnan(got), np.isnan(ref))
+    np.testing.assert_array_equal(got[~np.isnan(ref)], ref[~np.isnan(ref)])
