@@ -109,7 +109,25 @@ typedef struct hegrid_opts {
                                free at build time), > 0 = at most this many bytes, < 0 = never
                                (weights computed in every launch).  A plan whose image did not
                                fit retries on later calls. */
+    int32_t index;          /* hegrid_index: the plan's spatial index */
+    int32_t reserved;       /* must be 0 */
 } hegrid_opts;
+
+/* Spatial index of a plan (the LUT of PAPER.md:177-192, sec. 3.1.1, Fig. 4/5).
+ * BINS: map-aligned lon/lat bins, one per cell (rows of bins are contiguous sample ranges);
+ *       feeds the tensor-core and SIMT engines; fields reaching within ~1 degree of a pole,
+ *       spanning >= 180 degrees of longitude or with R > 1 degree are HEGRID_EUNSUPPORTED.
+ * HEALPIX: the paper's own index: samples sorted by HEALPix ring-scheme pixel (Gorski et
+ *       al. 2005); a cell gathers ring by ring over the pixel ranges that can
+ *       reach it (Algorithm 1) with an fp64 distance test and fp64 sums.
+ *       Any field, including polar caps and the whole sky; one gather kernel (the engine
+ *       option is ignored).
+ * AUTO: BINS where supported, else HEALPIX. */
+typedef enum hegrid_index {
+    HEGRID_INDEX_AUTO = 0,
+    HEGRID_INDEX_BINS = 1,
+    HEGRID_INDEX_HEALPIX = 2
+} hegrid_index;
 
 /* Value layouts accepted by hegrid_grid_device / hegrid_permute_device. */
 typedef enum hegrid_layout {
@@ -140,6 +158,8 @@ typedef struct hegrid_plan_stats {
     int64_t tc_block_slots;     /* (entry, in-reach 4x4-cell block) pairs: each is one
                                    16-cell x 32-sample slot of the dense MMA product, so
                                    n_pairs / (512 tc_block_slots) is the useful MMA density */
+    int32_t index;              /* hegrid_index the plan was built with (BINS or HEALPIX) */
+    int32_t nside;              /* HEALPIX: HEALPix resolution parameter (0 for BINS) */
 } hegrid_plan_stats;
 
 /* ---- plan: spatial index (PAPER.md:177-192 steps 1,2,4; Algorithm 1 region lookup) ----
@@ -213,6 +233,15 @@ hegrid_status hegrid_neighbours(hegrid_plan_t plan, int64_t cell_begin, int64_t 
 /* Stable LSD radix sort used by the plan, exposed for testing: perm = stable argsort of
  * host keys[n] (u32), computed on device `device`.  Blocking. */
 hegrid_status hegrid_sort_u32(const uint32_t* keys, int64_t n, int32_t* perm, int32_t device);
+
+/* HEALPix ring-scheme pixel index of n directions (the plan's HEALPIX key, computed on the
+ * device with the same code): pix[k] = ang2pix_ring(nside, theta[k], phi[k]), theta the
+ * colatitude in [0, pi] and phi the longitude in radians (any value; taken modulo 2 pi).
+ * Host arrays of n elements, borrowed for the call.  nside a power of two in [1, 8192];
+ * returns HEGRID_EINVAL otherwise, HEGRID_EDOMAIN for a non-finite or out-of-range theta.
+ * Exposed so the index can be checked against an independent implementation. */
+hegrid_status hegrid_healpix_ang2pix(int32_t nside, const double* theta, const double* phi,
+                                     int64_t n, int64_t* pix, int32_t device);
 
 /* Kernel-time profiling of the accumulate kernel: when enabled, hegrid_grid_device
  * brackets each accumulate launch with CUDA events on the caller's stream;

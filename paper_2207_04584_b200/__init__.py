@@ -16,7 +16,7 @@ from ._binding import (HEGRID_ENGINE_TC, HEGRID_LAYOUT_PLAN_NC, HEGRID_LAYOUT_US
                        hegrid_pipeline_trace, hegrid_plan_info, hegrid_plan_permutation,
                        hegrid_profile_enable,
                        hegrid_profile_read, hegrid_sort_u32, hegrid_status_string, make_map,
-                       make_opts)
+                       make_opts, hegrid_healpix_ang2pix, INDEXES)
 from .shard import channel_shard  # noqa: F401
 
 __all__ = ["Plan", "abi", "channel_shard", "HegridError"]
@@ -43,12 +43,12 @@ class Plan:
 
     def __init__(self, lon, lat, map, fwhm_deg, support_sigma=3.0, device=0, n_streams=0,
                  channel_block=0, stream=None, engine="auto", kernel="gaussian",
-                 weight_image_max_bytes=0):
+                 weight_image_max_bytes=0, index="auto"):
         self.map = dict(map) if isinstance(map, dict) else map
         self.nx, self.ny = int(self.map["nx"]), int(self.map["ny"])
         self.device = device
         opts = make_opts(device, n_streams, channel_block, self.ENGINES[engine],
-                         weight_image_max_bytes)
+                         weight_image_max_bytes, INDEXES[index])
         if hasattr(lon, "is_cuda") and lon.is_cuda:
             import torch
             lon = lon.to(torch.float64).contiguous()

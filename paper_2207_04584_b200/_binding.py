@@ -49,7 +49,8 @@ KERNELS = {"gaussian": HEGRID_KERNEL_GAUSSIAN, "tophat": HEGRID_KERNEL_TOPHAT}
 class hegrid_opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("n_streams", ctypes.c_int32),
                 ("channel_block", ctypes.c_int32), ("engine", ctypes.c_int32),
-                ("weight_image_max_bytes", ctypes.c_int64)]
+                ("weight_image_max_bytes", ctypes.c_int64), ("index", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class hegrid_plan_stats(ctypes.Structure):
@@ -61,7 +62,8 @@ class hegrid_plan_stats(ctypes.Structure):
                 ("ncol", ctypes.c_int32), ("mlat", ctypes.c_int32), ("mlon", ctypes.c_int32),
                 ("sigma_deg", ctypes.c_double), ("radius_deg", ctypes.c_double),
                 ("weight_image_bytes", ctypes.c_int64), ("tc_entries", ctypes.c_int64),
-                ("tc_block_slots", ctypes.c_int64)]
+                ("tc_block_slots", ctypes.c_int64), ("index", ctypes.c_int32),
+                ("nside", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -88,6 +90,7 @@ SIGNATURES = {
     "hegrid_permute_device": (I32, [PLAN, P, I64, I64, P, I64, P]),
     "hegrid_neighbours": (I32, [PLAN, I64, I64, P, P]),
     "hegrid_sort_u32": (I32, [P, I64, P, I32]),
+    "hegrid_healpix_ang2pix": (I32, [I32, P, P, I64, P, I32]),
     "hegrid_profile_enable": (I32, [PLAN, I32]),
     "hegrid_profile_read": (I32, [PLAN, P, P]),
     "hegrid_pipeline_trace": (I32, [PLAN, P, I64, P]),
@@ -147,9 +150,13 @@ def make_map(m) -> hegrid_map:
                       float(g("cdelt_lat")))
 
 
+HEGRID_INDEX_AUTO, HEGRID_INDEX_BINS, HEGRID_INDEX_HEALPIX = 0, 1, 2
+INDEXES = {"auto": HEGRID_INDEX_AUTO, "bins": HEGRID_INDEX_BINS, "healpix": HEGRID_INDEX_HEALPIX}
+
+
 def make_opts(device=0, n_streams=0, channel_block=0, engine=0,
-              weight_image_max_bytes=0) -> hegrid_opts:
-    return hegrid_opts(device, n_streams, channel_block, engine, weight_image_max_bytes)
+              weight_image_max_bytes=0, index=HEGRID_INDEX_AUTO) -> hegrid_opts:
+    return hegrid_opts(device, n_streams, channel_block, engine, weight_image_max_bytes, index, 0)
 
 
 # ----------------------------------------------------------------- C-ABI names
@@ -231,6 +238,18 @@ def hegrid_sort_u32(keys: np.ndarray, device: int = 0) -> np.ndarray:
     perm = np.empty(k.shape[0], np.int32)
     _check(load().hegrid_sort_u32(_ptr(k), k.shape[0], _ptr(perm), device), "hegrid_sort_u32")
     return perm
+
+
+def hegrid_healpix_ang2pix(nside: int, theta: np.ndarray, phi: np.ndarray, device: int = 0) -> np.ndarray:
+    """Ring-scheme pixel of each (colatitude, longitude) in radians, on the device."""
+    t = np.ascontiguousarray(theta, np.float64)
+    f = np.ascontiguousarray(phi, np.float64)
+    if t.shape != f.shape or t.ndim != 1:
+        raise ValueError("theta/phi must be equal-length 1-D arrays")
+    pix = np.empty(t.shape[0], np.int64)
+    _check(load().hegrid_healpix_ang2pix(nside, _ptr(t), _ptr(f), t.shape[0], _ptr(pix), device),
+           "hegrid_healpix_ang2pix")
+    return pix
 
 
 def hegrid_profile_enable(plan: int, enable: bool = True) -> None:

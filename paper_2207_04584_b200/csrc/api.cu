@@ -7,6 +7,9 @@
 
 #include <algorithm>
 #include <thread>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -72,6 +75,7 @@ static hegrid_status validate_geometry(const hegrid_map* m, const hegrid_kernel*
 static hegrid_opts default_opts(const hegrid_opts* o) {
     hegrid_opts r{};
     if (o) r = *o;
+    if (r.index < HEGRID_INDEX_AUTO || r.index > HEGRID_INDEX_HEALPIX) r.index = -1;   // rejected below
     if (r.n_streams <= 0) r.n_streams = 2;
     if (r.n_streams > 8) r.n_streams = 8;
     if (r.channel_block < 0) r.channel_block = 0;
@@ -96,13 +100,29 @@ static hegrid_status create_common(const double* d_lon, const double* d_lat, int
             return cuda_status(e);
         }
     }
-    hegrid_status s = build_plan(p, d_lon, d_lat, st);
+    // the spatial index: lon/lat bins where they serve the field, else (AUTO) or on request
+    // the HEALPix ring-scheme LUT (hpx.cu)
+    hegrid_status s = HEGRID_EUNSUPPORTED;
+    if (o.index != HEGRID_INDEX_HEALPIX) s = build_plan(p, d_lon, d_lat, st);
+    if ((s == HEGRID_EUNSUPPORTED && o.index == HEGRID_INDEX_AUTO) || o.index == HEGRID_INDEX_HEALPIX) {
+        p->index = HEGRID_INDEX_HEALPIX;
+        s = build_plan_hpx(p, d_lon, d_lat, st);
+    }
     if (s != HEGRID_OK) {
         hegrid_plan_destroy(p);
         return s;
     }
     *out = p;
     return HEGRID_OK;
+}
+
+void phase_mark(const char* what) {
+    static const bool on = getenv("HEGRID_TIMING") != nullptr;
+    static auto t0 = std::chrono::steady_clock::now();
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[hegrid] %-32s %9.2f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
 }
 
 cudaError_t shared_pool(int device, cudaMemPool_t* pool) {
@@ -131,7 +151,8 @@ cudaError_t shared_pool(int device, cudaMemPool_t* pool) {
 }
 
 hegrid_status prepare_engine(const hegrid_plan_s* p, int64_t n_channels_per_launch) {
-    if (p->opts.engine == HEGRID_ENGINE_SIMT || p->n_used == 0) return HEGRID_OK;
+    if (p->index == HEGRID_INDEX_HEALPIX || p->opts.engine == HEGRID_ENGINE_SIMT || p->n_used == 0)
+        return HEGRID_OK;
     auto* q = const_cast<hegrid_plan_s*>(p);
     if (!q->prep_st) HG_TRY(cudaStreamCreateWithFlags(&q->prep_st, cudaStreamNonBlocking));
     return prepare_tc(p, n_channels_per_launch, q->prep_st);
@@ -140,8 +161,11 @@ hegrid_status prepare_engine(const hegrid_plan_s* p, int64_t n_channels_per_laun
 hegrid_status launch_accumulate(const hegrid_plan_s* p, const float* d_v, int64_t ldv,
                                 int64_t n_channels, float* d_out, float* d_weight,
                                 cudaStream_t st) {
-    // AUTO takes the tensor-core engine: faster on every measured configuration (DESIGN.md
+    // HEALPix-indexed plans have their own gather (Algorithm 1, hpx.cu).  Otherwise AUTO
+    // takes the tensor-core engine: faster on every measured configuration (DESIGN.md
     // section 11: cfg2 1.5 vs 4.4 ms, cfg3 7.3 vs 109 ms, cfg4 14 vs 68 ms)
+    if (p->index == HEGRID_INDEX_HEALPIX)
+        return launch_accumulate_hpx(p, d_v, ldv, n_channels, d_out, d_weight, st);
     if (p->opts.engine == HEGRID_ENGINE_SIMT)
         return launch_accumulate_simt(p, d_v, ldv, n_channels, d_out, d_weight, st);
     return launch_accumulate_tc(p, d_v, ldv, n_channels, d_out, d_weight, st);
@@ -177,12 +201,15 @@ hegrid_status hegrid_plan_create(const double* lon_deg, const double* lat_deg, i
     if (n > 0 && (!lon_deg || !lat_deg)) return HEGRID_EINVAL;
     HG_TRY_S(validate_geometry(map, kernel));
     hegrid_opts o = default_opts(opts);
+    if (o.index < 0 || o.reserved != 0) return HEGRID_EINVAL;
     DeviceGuard dg(o.device);
     HG_TRY(dg.err);
     // coordinates H2D into stream-ordered buffers of the device pool (no cudaMalloc / cudaFree
     // and their device-wide synchronisation on the plan path)
+    phase_mark("plan_create: enter");
     cudaMemPool_t pool = nullptr;
     HG_TRY(shared_pool(o.device, &pool));
+    phase_mark("plan_create: pool");
     cudaStream_t st = nullptr;
     HG_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     double *d_lon = nullptr, *d_lat = nullptr;
@@ -192,11 +219,14 @@ hegrid_status hegrid_plan_create(const double* lon_deg, const double* lat_deg, i
     if (e == cudaSuccess && n > 0) e = cudaMemcpyAsync(d_lon, lon_deg, n * 8, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess && n > 0) e = cudaMemcpyAsync(d_lat, lat_deg, n * 8, cudaMemcpyHostToDevice, st);
     hegrid_status s = cuda_status(e);
+    phase_mark("plan_create: coords H2D");
     if (s == HEGRID_OK) s = create_common(d_lon, d_lat, n, map, kernel, o, st, out);
+    phase_mark("plan_create: build");
     if (d_lon) cudaFreeAsync(d_lon, st);
     if (d_lat) cudaFreeAsync(d_lat, st);
     cudaError_t e2 = cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
+    phase_mark("plan_create: done");
     if (s == HEGRID_OK && e2 != cudaSuccess) {
         hegrid_plan_destroy(*out);
         *out = nullptr;
@@ -213,6 +243,7 @@ hegrid_status hegrid_plan_create_device(const double* d_lon, const double* d_lat
     if (n > 0 && (!d_lon || !d_lat)) return HEGRID_EINVAL;
     HG_TRY_S(validate_geometry(map, kernel));
     hegrid_opts o = default_opts(opts);
+    if (o.index < 0 || o.reserved != 0) return HEGRID_EINVAL;
     DeviceGuard dg(o.device);
     HG_TRY(dg.err);
     return create_common(d_lon, d_lat, n, map, kernel, o, (cudaStream_t)stream, out);
@@ -221,6 +252,7 @@ hegrid_status hegrid_plan_create_device(const double* d_lon, const double* d_lat
 void hegrid_plan_destroy(hegrid_plan_t p) {
     if (!p) return;
     DeviceGuard dg(p->device);
+    phase_mark("plan_destroy: enter");
     // the plan's arrays go back to the device pool once all work issued so far is done
     cudaDeviceSynchronize();
     for (void* q : {(void*)p->d_keys, (void*)p->d_perm, (void*)p->d_iperm, (void*)p->d_geo,
@@ -240,6 +272,7 @@ void hegrid_plan_destroy(hegrid_plan_t p) {
     if (p->prep_st) cudaStreamDestroy(p->prep_st);
     cudaStreamSynchronize(0);
     delete p;
+    phase_mark("plan_destroy: done");
 }
 
 hegrid_status hegrid_plan_info(hegrid_plan_t p, hegrid_plan_stats* out) {
@@ -247,7 +280,8 @@ hegrid_status hegrid_plan_info(hegrid_plan_t p, hegrid_plan_stats* out) {
     DeviceGuard dg(p->device);
     HG_TRY(dg.err);
     if (!p->stats_valid) {
-        HG_TRY_S(plan_pair_stats(p, 0));
+        if (p->index == HEGRID_INDEX_HEALPIX) HG_TRY_S(hpx_pair_stats(p, 0));
+        else HG_TRY_S(plan_pair_stats(p, 0));
         p->stats_valid = true;
     }
     hegrid_plan_stats s = p->stats;
@@ -262,6 +296,8 @@ hegrid_status hegrid_plan_info(hegrid_plan_t p, hegrid_plan_stats* out) {
     s.sigma_deg = p->g.sigma_rad / kDeg2Rad;
     s.radius_deg = p->g.R_rad / kDeg2Rad;
     s.weight_image_bytes = p->tc_pw == 1 ? p->tc_wimg_bytes : 0;
+    s.index = p->index;
+    s.nside = p->hpx_nside;
     s.tc_entries = p->tc_nchunks > 0 ? p->tc_nchunks : 0;
     s.tc_block_slots = p->tc_nchunks > 0 ? (int64_t)p->tc_stats[1] : 0;
     *out = s;
@@ -513,8 +549,10 @@ hegrid_status hegrid_neighbours(hegrid_plan_t p, int64_t cell_begin, int64_t cel
     if (cell_begin < 0 || cell_end < cell_begin || cell_end > cells) return HEGRID_EINVAL;
     DeviceGuard dg(p->device);
     HG_TRY(dg.err);
-    // the pairs of the engine that grids: the tensor-core engine's chunk schedule (the
-    // default), or the SIMT engine's per-cell candidate ranges
+    // the pairs of the engine that grids: the HEALPix gather's ring ranges, the tensor-core
+    // engine's chunk schedule (the default), or the SIMT engine's per-cell candidate ranges
+    if (p->index == HEGRID_INDEX_HEALPIX)
+        return hpx_neighbours(p, cell_begin, cell_end, offsets, sample_idx, 0);
     if (p->opts.engine == HEGRID_ENGINE_SIMT)
         return plan_neighbours(p, cell_begin, cell_end, offsets, sample_idx, 0);
     return tc_neighbours(p, cell_begin, cell_end, offsets, sample_idx, 0);

@@ -60,6 +60,8 @@ struct PlanDev {
 
 struct hegrid_plan_s {
     int device = 0;
+    int index = HEGRID_INDEX_BINS;   // the plan's spatial index (hegrid_index)
+    int hpx_nside = 0;               // HEALPIX: resolution of the ring-scheme keys (hpx.cu)
     hegrid_map map{};
     hegrid_kernel kern{};
     hegrid_opts opts{};
@@ -133,6 +135,16 @@ hegrid_status plan_pair_stats(hegrid_plan_s* p, cudaStream_t st);
 hegrid_status plan_neighbours(hegrid_plan_s* p, int64_t c0, int64_t c1, int64_t* offsets,
                               int64_t* idx, cudaStream_t st);
 
+// hpx.cu (HEALPix-indexed plans)
+hegrid_status build_plan_hpx(hegrid_plan_s* p, const double* d_lon, const double* d_lat,
+                             cudaStream_t st);
+hegrid_status launch_accumulate_hpx(const hegrid_plan_s* p, const float* d_v, int64_t ldv,
+                                    int64_t n_channels, float* d_out, float* d_weight,
+                                    cudaStream_t st);
+hegrid_status hpx_neighbours(const hegrid_plan_s* p, int64_t c0, int64_t c1, int64_t* offsets,
+                             int64_t* idx, cudaStream_t st);
+hegrid_status hpx_pair_stats(hegrid_plan_s* p, cudaStream_t st);
+
 // grid_simt.cu
 hegrid_status launch_accumulate_simt(const hegrid_plan_s* p, const float* d_v, int64_t ldv,
                                      int64_t n_channels, float* d_out, float* d_weight,
@@ -156,6 +168,9 @@ cudaError_t shared_pool(int device, cudaMemPool_t* pool);
 // grid_tc.cu / api.cu: build the engine's per-plan tables now (on the plan's prep stream)
 hegrid_status prepare_engine(const hegrid_plan_s* p, int64_t n_channels_per_launch);
 hegrid_status prepare_tc(const hegrid_plan_s* p, int64_t n_channels_per_launch, cudaStream_t st);
+
+// HEGRID_TIMING=1: host-side phase timer (stderr), for the one-time plan / engine costs
+void phase_mark(const char* what);
 
 inline cudaError_t plan_alloc(const hegrid_plan_s* p, void* ptr, size_t bytes, cudaStream_t st) {
     return cudaMallocFromPoolAsync(reinterpret_cast<void**>(ptr), bytes, p->pool, st);
