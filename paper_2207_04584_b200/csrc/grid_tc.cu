@@ -17,22 +17,21 @@
 //     PAPER.md:209-217, hoisted out of the hot loop);
 //   * W per cell, summed by k_tc_wsum from the very same fp32 weights (patch_weights).
 //
-// CTA = 16x16 cells (16 blocks) x 128 channels, 512 threads, warp-specialised:
-//   warp 0 (lane 0) : MMA issuer: per chunk, per run of consecutive in-reach blocks, 4 K-steps
-//                     x 3 MMAs with N = 16 r; commits free the A and B stages;
-//   warp 1          : V loader: cp.async.bulk of the chunk's value rows (512 B each) into a
-//                     4-stage shared ring, completion as mbarrier tx bytes;
-//   warps 4-7       : A producers (thread = channel = TMEM lane): split the staged values
-//                     and tcgen05.st them into one of 4 TMEM stages; in dense mode they
-//                     also move D out every `promote_every` chunks (see below);
-//   warps 8-15      : B producers: thread = (cell row, 4-sample quad, slots q0, q0+8),
-//                     geometry prefetched ahead; weights to one of 2 shared stages laid out
-//                     so that consecutive slots form one K-major operand of N = 16 r.
-//   dense mode      : every `promote_every` chunks the A producers add D into the CTA's
-//                     own (exclusively owned) out_map slice and the issuer restarts D,
-//                     bounding the tensor-core accumulations (not fp32 round-to-nearest)
-//                     behind any partial sum.
-// Epilogue: tcgen05.ld of D, V = S / W (IEEE div), NaN where W = 0.
+// k_accum_tc: CTA = 16x12 cells (12 blocks of 4x4) x 128 channels, 512 threads in roles:
+//   MMA issuers (warps 0, 3, and 13 with precomputed weights): issuer i issues the MMAs of
+//                     the block rows r with r % NI == i: per run of consecutive in-reach
+//                     blocks, 4 K-steps x 3 products (N = 16 r), one commit per chunk;
+//   warp 1          : value loader: one 2D TMA box (32 plan rows x 128 channels) per chunk
+//                     into a 3-stage ring (+ the chunk's geometry in on-the-fly mode);
+//   warp 2 (PW)     : weight loader: the chunk's precomputed weight-image bytes into a ring;
+//   A producers     : (thread = channel = TMEM lane) split the staged values into tf32 hi/lo
+//                     and tcgen05.st them into one of 2 TMEM A stages; every SEG chunks they
+//                     add the finished D buffer into the fp32 master tile in shared memory
+//                     (D is double-buffered in TMEM, round-to-nearest promotion bounds the
+//                     tensor core's truncating accumulation);
+//   B producers (OTF): compute the chunk's weights into 2 shared weight stages.
+// Epilogue: the last segments are promoted, V = S / W (IEEE div), NaN where W = 0, written as
+// coalesced row segments.  The persistent variant k_accum_pw is described further down.
 // Deterministic: fixed chunk order, fixed work mapping, no atomics.
 #include <stdio.h>
 #include <stdlib.h>
@@ -152,6 +151,7 @@ struct TcSmem {
     uint4 Es[NV];                         // the chunk's schedule entry (written by the V loader)
     uint32_t Bmask[NBF];                  // block mask of the chunk in each weight stage / ring entry
     uint32_t Boff[NBF];                   // PW: ring offset of the entry
+    long long Wstart[NBF];                // PW weight loader: ring position of each in-flight entry
     // chunk c: A stage c % NA, B stage c % NBS (OTF) or ring entry c % NBF (PW)
     uint64_t a_full[NA], b_full[NBF], done[NBF], v_full[NV], v_empty[NV];
     uint64_t seg_done[2], seg_free[2];    // D buffer d: segment's MMAs complete / promoted
@@ -829,29 +829,6 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                                                            tc::idesc_tf32(TC_M, nw));
                     }
                 }
-#if defined(HG_TC_MMA36)
-                static_assert(KA == 1, "36-MMA issue for 32-sample chunks");
-                while (mm) {                       // up to three runs per asm block
-                    uint32_t dd[3] = {0, 0, 0}, bb[3] = {0, 0, 0}, ii[3] = {0, 0, 0};
-                    int nr = 0;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        if (mm) {
-                            const int b = __ffs(mm) - 1;
-                            const int r = __ffs(~(mm >> b)) - 1;
-                            mm &= ~(((1u << r) - 1u) << b);
-                            const int q = __popc(mask & ((1u << b) - 1u));
-                            dd[k] = dbase + (uint32_t)(b * TC_N);
-                            bb[k] = dh0 + (uint32_t)((q * ATOM_SLOT) >> 4);
-                            ii[k] = tc::idesc_tf32(TC_M, TC_N * r);
-                            nr = k + 1;
-                        }
-                    }
-                    tc::mma36_3xtf32<(32 >> 4), TC_KC>(a0, dd[0], bb[0], bb[0] + (uint32_t)lo16, ii[0],
-                                                       dd[1], bb[1], bb[1] + (uint32_t)lo16, ii[1],
-                                                       dd[2], bb[2], bb[2] + (uint32_t)lo16, ii[2], nr);
-                }
-#else
                 while (mm) {
                     const int b = __ffs(mm) - 1;
                     const int r = __ffs(~(mm >> b)) - 1;
@@ -864,7 +841,6 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                                                            bh + (uint32_t)lo16, tc::idesc_tf32(TC_M, TC_N * r));
                     }
                 }
-#endif
             }
             if (dbg & 4096) {                          // debug (with no MMAs): plain arrive
                 __syncwarp();
@@ -899,7 +875,10 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         // one bulk copy of the 32 geometry records per chunk, L2 prefetch PF chunks ahead
         // schedule entries: the warp loads 32 at a time (lane l holds entry c0 + l), one
         // batch ahead, and hands each chunk's entry to the consumers through Es[stage]
-        constexpr int PF = NV + 3;
+#ifndef HG_TC_PFX
+#define HG_TC_PFX 3
+#endif
+        constexpr int PF = NV + HG_TC_PFX;
         static_assert(PF < 32, "prefetch distance must stay within the next entry batch");
         auto ld_entry = [&](int c) { return c < nchunks ? __ldg(&cs[ent(c)]) : make_uint4(0, 0, 0, 0); };
         uint4 cur = ld_entry(lane), nxt = ld_entry(32 + lane);
@@ -975,14 +954,19 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             ldg(2 * G, zf, sf);
             pf(zc, sc);
             pf(zn, sn);
-            long long head = 0, starts[NBF];
+            long long head = 0;
+            long long* starts = sm.Wstart;    // (shared, not a local-memory array)
             int conf = 0;                         // chunks confirmed complete
             for (int g0 = 0; g0 < nchunks; g0 += G) {
 #pragma unroll
                 for (int u = 0; u < G; ++u) {
                     const int c = g0 + u;
                     if (c >= nchunks) break;
+#ifdef HG_TC_HALFW
+                    const uint32_t bytes = (dbg & 2048) ? 0u : __popc(zc[u]) * 1u * SLOT_BYTES;   // timing experiment
+#else
                     const uint32_t bytes = (dbg & 2048) ? 0u : __popc(zc[u]) * 2u * SLOT_BYTES;
+#endif
                     long long off = head % RING;
                     if (off + bytes > RING) {
                         head += RING - off;
@@ -1514,7 +1498,11 @@ k_accum_pw(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 #endif
                         PTL(4);
                         // ---- weight bytes
+#ifdef HG_TC_HALFW
+                        const uint32_t bytes = __popc(e.z) * 1u * SLOT_BYTES;   // timing experiment
+#else
                         const uint32_t bytes = __popc(e.z) * 2u * SLOT_BYTES;
+#endif
                         long long off = head % PW_RING;
                         if (off + bytes > PW_RING) {
                             head += PW_RING - off;

@@ -84,31 +84,6 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n\t"
         "}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
-// Wait with exponential nanosleep backoff (64 .. 512 ns): for roles whose waits are long and
-// off the critical path (the promoters wait a whole segment).  A try_wait with a suspend hint
-// wakes on every mbarrier event of the CTA, so a dozen warps parked in it keep re-issuing the
-// wait loop (measured: ~1 issue slot per cycle per SM taken from the pipeline roles).
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t"
-        ".reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t"
-        "}\n" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
-    uint32_t ns = 64;
-    while (!mbar_test(bar, parity)) {
-        __nanosleep(ns);
-        ns = ns < 512 ? 2 * ns : 512;
-    }
-}
-// Kept for the roles that usually run ahead (same wait; the hint already suspends).
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-    mbar_wait(bar, parity);
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
 }
@@ -140,73 +115,6 @@ __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
 }
 
 // ---- MMA ---------------------------------------------------------------------------
-// D[tmem] (+)= A[tmem] * B[smem desc]^T, kind::tf32, cta_group::1.
-__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                            uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t"
-        ".reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
-        "}\n" :: "r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
-}
-// Warp-uniform variant: the whole (converged) warp executes it with uniform operands and
-// one elected lane issues, which avoids the per-MMA uniformisation loop the compiler
-// generates for a single-lane branch (~25 vs ~76 cycles per MMA measured on B200).
-__device__ __forceinline__ void mma_tf32_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                                 uint32_t idesc) {
-    asm volatile(
-        "{\n\t"
-        ".reg .pred p, e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "setp.ne.b32 p, 1, 0;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
-        "}\n" :: "r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc));
-}
-__device__ __forceinline__ void mma_tf32_ts_warp_acc(uint32_t d_tmem, uint32_t a_tmem,
-                                                     uint64_t b_desc, uint32_t idesc,
-                                                     uint32_t accumulate) {
-    asm volatile(
-        "{\n\t"
-        ".reg .pred p, e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
-        "}\n" :: "r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
-}
-// One run of the 3xTF32 product over a 32-sample chunk: 4 K-steps x (hi*hi, hi*lo, lo*hi),
-// 12 MMAs behind a single elect.  A stage in TMEM: hi at columns a0 + 8 ks, lo at
-// a0 + 32 + 8 ks; B descriptors: hi at b0 + ks * KS_STEP (16-B units), lo at + lo_off.
-// The first MMA accumulates iff acc0 != 0, the other 11 always accumulate.
-template <int KS_STEP>
-__device__ __forceinline__ void mma_run_3xtf32(uint32_t d, uint32_t a0, uint64_t b0,
-                                               uint64_t lo_off, uint32_t idesc, uint32_t acc0) {
-#define HG_MMA_KS(ka, kl, bo)                                                              \
-    "add.u32 ah, %1, " #ka ";\n\t"                                                         \
-    "add.u32 al, %1, " #kl ";\n\t"                                                         \
-    "add.s64 bh, %2, %" #bo ";\n\t"                                                        \
-    "add.s64 bl, bh, %5;\n\t"                                                              \
-    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bh, %3, t;\n\t"                    \
-    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bl, %3, t;\n\t"                    \
-    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], bh, %3, t;\n\t"
-    asm volatile(
-        "{\n\t"
-        ".reg .pred e, p, t;\n\t"
-        ".reg .b32 ah, al;\n\t"
-        ".reg .b64 bh, bl;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "setp.eq.u32 t, 0, 0;\n\t"
-        "add.s64 bl, %2, %5;\n\t"
-        "add.u32 al, %1, 32;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], bl, %3, t;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], %2, %3, t;\n\t"
-        HG_MMA_KS(8, 40, 6) HG_MMA_KS(16, 48, 7) HG_MMA_KS(24, 56, 8)
-        "}\n" :: "r"(d), "r"(a0), "l"(b0), "r"(idesc), "r"(acc0), "l"(lo_off),
-        "n"(KS_STEP), "n"(2 * KS_STEP), "n"(3 * KS_STEP));
-#undef HG_MMA_KS
-}
 // The same 12 MMAs issued so that ptxas keeps the operand arithmetic in uniform registers:
 // TMEM operands as [base + immediate] (A hi at a0 + 8 ks, lo at a0 + 32 + 8 ks) and the B
 // descriptors built inside the asm from their low words (start address, LBO) with the
@@ -287,53 +195,6 @@ __device__ __forceinline__ void mma12_3xtf32_acc(uint32_t d, uint32_t a0, uint32
         "n"(ALO + 16), "n"(ALO + 24), "r"(acc0) : "memory");
 #undef HG_MMA12A_KS
 }
-// Up to three runs of one chunk (4 K-steps x 3 products each, 36 MMAs) behind one elect:
-// runs 1 and 2 are predicated on nr > 1, nr > 2.  Every operand base enters the asm once
-// (D, B-descriptor low words, instruction descriptor per run; one A base), so ptxas moves
-// each to a uniform register once per chunk instead of once per MMA.
-template <int KS_STEP, int ALO = 32>
-__device__ __forceinline__ void mma36_3xtf32(uint32_t a0, uint32_t d0, uint32_t bh0, uint32_t bl0,
-                                             uint32_t i0, uint32_t d1, uint32_t bh1, uint32_t bl1,
-                                             uint32_t i1, uint32_t d2, uint32_t bh2, uint32_t bl2,
-                                             uint32_t i2, int nr) {
-#define HG_MMA36_RUN(P, D, BH, BL, ID)                                                         \
-    "add.u32 x1, " BH ", %13;\n\t" "add.u32 x2, " BH ", %14;\n\t" "add.u32 x3, " BH ", %15;\n\t" \
-    "add.u32 y1, " BL ", %13;\n\t" "add.u32 y2, " BL ", %14;\n\t" "add.u32 y3, " BL ", %15;\n\t" \
-    "mov.b64 h0, {" BH ", %16};\n\t" "mov.b64 h1, {x1, %16};\n\t"                              \
-    "mov.b64 h2, {x2, %16};\n\t" "mov.b64 h3, {x3, %16};\n\t"                                  \
-    "mov.b64 l0, {" BL ", %16};\n\t" "mov.b64 l1, {y1, %16};\n\t"                              \
-    "mov.b64 l2, {y2, %16};\n\t" "mov.b64 l3, {y3, %16};\n\t"                                  \
-    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0], h0, " ID ", 1;\n\t"                 \
-    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0], l0, " ID ", 1;\n\t"                 \
-    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+%17], h0, " ID ", 1;\n\t"             \
-    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+8], h1, " ID ", 1;\n\t"               \
-    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+8], l1, " ID ", 1;\n\t"               \
-    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+%18], h1, " ID ", 1;\n\t"             \
-    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+16], h2, " ID ", 1;\n\t"              \
-    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+16], l2, " ID ", 1;\n\t"              \
-    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+%19], h2, " ID ", 1;\n\t"             \
-    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+24], h3, " ID ", 1;\n\t"              \
-    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+24], l3, " ID ", 1;\n\t"              \
-    "@" P " tcgen05.mma.cta_group::1.kind::tf32 [" D "], [%0+%20], h3, " ID ", 1;\n\t"
-    asm volatile(
-        "{\n\t"
-        ".reg .pred e, e1, e2, q1, q2;\n\t"
-        ".reg .b32 x1, x2, x3, y1, y2, y3;\n\t"
-        ".reg .b64 h0, h1, h2, h3, l0, l1, l2, l3;\n\t"
-        "setp.gt.s32 q1, %21, 1;\n\t"
-        "setp.gt.s32 q2, %21, 2;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "and.pred e1, e, q1;\n\t"
-        "and.pred e2, e, q2;\n\t"
-        HG_MMA36_RUN("e", "%1", "%2", "%3", "%4")
-        HG_MMA36_RUN("e1", "%5", "%6", "%7", "%8")
-        HG_MMA36_RUN("e2", "%9", "%10", "%11", "%12")
-        "}\n" :: "r"(a0), "r"(d0), "r"(bh0), "r"(bl0), "r"(i0), "r"(d1), "r"(bh1), "r"(bl1),
-        "r"(i1), "r"(d2), "r"(bh2), "r"(bl2), "r"(i2), "n"(KS_STEP), "n"(2 * KS_STEP),
-        "n"(3 * KS_STEP), "n"(kDescHiSw128), "n"(ALO), "n"(ALO + 8), "n"(ALO + 16), "n"(ALO + 24),
-        "r"(nr) : "memory");
-#undef HG_MMA36_RUN
-}
 // low word of a K-major SWIZZLE_128B descriptor (start address >> 4, LBO field 1)
 __device__ __forceinline__ uint32_t sdesc_sw128_lo(uint32_t saddr) {
     return ((saddr >> 4) & 0x3FFFu) | (1u << 16);
@@ -346,12 +207,6 @@ __device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
         "}\n" :: "r"(smem_u32(bar)) : "memory");
 }
-// Arrives on `bar` when all previously issued MMAs of this thread have completed.
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                 :: "r"(smem_u32(bar)) : "memory");
-}
-
 // Instruction descriptor: kind::tf32, D fp32, A/B tf32 K-major, M x N.
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4)                          // c_format = F32
@@ -359,31 +214,6 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
          | (2u << 10)                         // b_format = TF32
          | ((uint32_t)(N >> 3) << 17)         // n_dim
          | ((uint32_t)(M >> 4) << 24);        // m_dim
-}
-
-// Shared-memory matrix descriptor, no swizzle (canonical K-major interleaved layout:
-// 8 rows x 16 B core matrices; LBO = byte distance between the two K core matrices of
-// one MMA, SBO = byte distance between 8-row groups).
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-    d |= (uint64_t)1 << 46;                   // version (sm_100)
-    return d;                                 // base offset 0, layout SWIZZLE_NONE (0)
-}
-
-// Shared-memory matrix descriptor, K-major with 128-byte swizzle: 8-row x 128-B atoms
-// (1024-B aligned), SBO = 1024 B between 8-row groups, LBO unused (1).  Advancing along K
-// inside the atom adds the byte offset (>> 4) to the start address.
-__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;                   // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;         // SBO
-    d |= (uint64_t)1 << 46;                   // version (sm_100)
-    d |= (uint64_t)2 << 61;                   // layout: SWIZZLE_128B
-    return d;
 }
 
 // ---- TMEM <-> registers (32 lanes x 32 bit, per warp) ------------------------------
@@ -433,13 +263,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
     hi = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
     lo = __float_as_uint(x - __uint_as_float(hi));
-}
-
-// fp32 -> tf32 (round to nearest, ties away), result kept in a 32-bit container
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
 }
 
 }  // namespace tc

@@ -3,7 +3,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
-#include "../paper_2207_04584_b200/csrc/tc_ptx.cuh"
+#include "tc_bench_ptx.cuh"
 using namespace hg;
 
 __device__ __forceinline__ uint64_t sdesc_mn128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {

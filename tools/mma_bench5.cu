@@ -4,7 +4,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
-#include "../paper_2207_04584_b200/csrc/tc_ptx.cuh"
+#include "tc_bench_ptx.cuh"
 using namespace hg;
 
 __device__ __forceinline__ void run12(uint32_t d, uint32_t a1, uint32_t a2, uint32_t a3, uint64_t b1, uint64_t b2, uint64_t b3, uint32_t idesc) {

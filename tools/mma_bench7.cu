@@ -4,7 +4,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
-#include "../paper_2207_04584_b200/csrc/tc_ptx.cuh"
+#include "tc_bench_ptx.cuh"
 using namespace hg;
 
 __global__ void k(int n, int nb, int iters, int cm, unsigned long long* out) {

@@ -7,10 +7,10 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
-#include "../paper_2207_04584_b200/csrc/tc_ptx.cuh"
+#include "tc_bench_ptx.cuh"
 using namespace hg;
 
-enum { F_MMA = 1, F_STTM = 2, F_VLDS = 4, F_VCP = 8, F_WCP = 16, F_PROMO = 32, F_SPIN = 64 };
+enum { F_MMA = 1, F_STTM = 2, F_VLDS = 4, F_VCP = 8, F_WCP = 16, F_PROMO = 32, F_SPIN = 64, F_HALFN = 128 };
 constexpr int NV = 3, NB = 4, NBF = 16, SEG = 16;
 constexpr uint32_t VST = 16384, WST = 16384;
 
@@ -235,8 +235,9 @@ __global__ void __launch_bounds__(512, 1) k2(const uint8_t* __restrict__ vsrc, c
                 const uint32_t b0 = wb + (c % NB2) * WST;
                 const uint32_t a0 = tm + AC0 + (c % NA) * 64;
                 const uint32_t db = tm + d * 96;
-                tc::mma12_3xtf32<2>(db + 0, a0, tc::sdesc_sw128_lo(b0), tc::sdesc_sw128_lo(b0 + 8192), tc::idesc_tf32(128, 32));
-                tc::mma12_3xtf32<2>(db + 64, a0, tc::sdesc_sw128_lo(b0 + 4096), tc::sdesc_sw128_lo(b0 + 12288), tc::idesc_tf32(128, 32));
+                const int nn = (F & F_HALFN) ? 16 : 32;
+                tc::mma12_3xtf32<2>(db + 0, a0, tc::sdesc_sw128_lo(b0), tc::sdesc_sw128_lo(b0 + 8192), tc::idesc_tf32(128, nn));
+                tc::mma12_3xtf32<2>(db + 64, a0, tc::sdesc_sw128_lo(b0 + 4096), tc::sdesc_sw128_lo(b0 + 12288), tc::idesc_tf32(128, nn));
             }
             tc::mma_commit_warp(&s.done[c % NBF]);
             if ((F & F_PROMO) && (c % SEG == SEG - 1 || c == E - 1)) tc::mma_commit_warp(&s.seg_done[d]);
@@ -371,6 +372,210 @@ void run2(const char* name, const uint8_t* v, const uint8_t* w, size_t span, uns
            NV2, NB2, NA, h[0] / (double)grid / E, ms * 1e-3 * 1.965e9 / E, e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
 
+
+// ---------------------------------------------------------------- V tile throughput: bulk vs 2D TMA box
+#include <cuda.h>
+__global__ void __launch_bounds__(128, 1) kv(const __grid_constant__ CUtensorMap tm, const uint8_t* __restrict__ src,
+                                              int mode, int E, int rows_total, int ncb, unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t raw[];
+    constexpr int NS = 6;
+    uint64_t* full = reinterpret_cast<uint64_t*>(raw + NS * VST);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NS; ++i) tc::mbar_init(&full[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const long long t0 = clock64();
+    if (warp == 0 && lane == 0) {
+        unsigned seed = blockIdx.x * 2654435761u;
+        for (int c = 0; c < E; ++c) {
+            const int s = c % NS;
+            if (c >= NS) tc::mbar_wait(&full[s], ((c / NS) - 1) & 1);
+            seed = seed * 1664525u + 1013904223u;
+            const int row = (int)((seed >> 8) % (unsigned)(rows_total - 32));
+            const int cb = (int)(blockIdx.x % ncb) * 128;
+            tc::mbar_arrive_expect_tx(&full[s], VST);
+            if (mode == 0) tc::tma_load_2d(raw + s * VST, &tm, cb, row, &full[s]);
+            else tc::bulk_g2s(raw + s * VST, src + ((size_t)(blockIdx.x % ncb) * rows_total + row) * 512, VST, &full[s]);
+        }
+        for (int c = E; c < E + NS; ++c) { const int s = c % NS; tc::mbar_wait(&full[s], ((c / NS) - 1) & 1); }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(&out[0], (unsigned long long)(clock64() - t0));
+}
+void run_v(int mode, const char* name, uint8_t* v, size_t span, unsigned long long* d) {
+    using encode_fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                   const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+    const int C = 4096, rows = (int)(span / (C * 4));
+    alignas(64) CUtensorMap tm;
+    const cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)C * 4};
+    const cuuint32_t box[2] = {128, 32};
+    const cuuint32_t es[2] = {1, 1};
+    ((encode_fn)f)(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, v, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const int E = 3000, grid = 148, sm = 6 * VST + 64;
+    cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    kv<<<grid, 128, sm>>>(tm, v, mode, E, mode == 0 ? rows : rows / 32 * 32, 32, d);
+    cudaMemset(d, 0, 8);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    kv<<<grid, 128, sm>>>(tm, v, mode, E, mode == 0 ? rows : rows / 32 * 32, 32, d);
+    cudaEventRecord(e1);
+    cudaError_t e = cudaDeviceSynchronize();
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    printf("%-40s %.1f cycles/tile, %.2f TB/s %s\n", name, ms * 1e-3 * 1.965e9 / E, 148.0 * E * VST / (ms * 1e-3) / 1e12,
+           e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
+
+// ---------------------------------------------------------------- k3: a half-size pipeline (256 threads,
+// 96 KB SMEM, 256 TMEM columns) to test 2 CTAs per SM.  Roles: W0 issuer, W1 V loader, W2 W loader,
+// W3 promoter (LDTM of the touched blocks every SEG entries), W4-7 A producers (32 samples / thread).
+struct Smem3 {
+    uint8_t W[3][WST];
+    uint8_t V[3][VST];
+    uint64_t a_full[2], b_full[3], v_full[3], v_empty[3], done[NBF], seg_done, seg_free;
+    uint32_t tbase;
+};
+template <int F>
+__global__ void __launch_bounds__(256) k3(const uint8_t* __restrict__ vsrc, const uint8_t* __restrict__ wsrc,
+                                          size_t span, size_t vspan, uint32_t wbytes, int E, int tcols,
+                                          unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t raw[];
+    Smem3& s = *reinterpret_cast<Smem3*>(raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NA = 2, NV3 = 3, NB3 = 3;
+    if (warp == 0) {
+        if (tcols == 256) tc::tmem_alloc(&s.tbase, 256); else tc::tmem_alloc(&s.tbase, 512);
+    }
+    if (threadIdx.x == 32) {
+        for (int i = 0; i < NA; ++i) tc::mbar_init(&s.a_full[i], 4);
+        for (int i = 0; i < NB3; ++i) tc::mbar_init(&s.b_full[i], 1);
+        for (int i = 0; i < NV3; ++i) { tc::mbar_init(&s.v_full[i], 1); tc::mbar_init(&s.v_empty[i], 4); }
+        for (int i = 0; i < NBF; ++i) tc::mbar_init(&s.done[i], 1);
+        tc::mbar_init(&s.seg_done, 1);
+        tc::mbar_init(&s.seg_free, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tm = s.tbase;
+    const long long t0 = clock64();
+    const size_t cta_off = (size_t)blockIdx.x * 7919 * 256;
+    if (warp == 0) {
+        const uint32_t wb = tc::smem_u32(&s.W[0][0]);
+        uint32_t gs = 0;
+        for (int c = 0; c < E; ++c) {
+            if (c % SEG == 0 && c > 0) { tc::mbar_wait(&s.seg_free, (gs - 1) & 1); tc::fence_after_sync(); }
+            tc::mbar_wait(&s.a_full[c % NA], (c / NA) & 1);
+            tc::mbar_wait(&s.b_full[c % NB3], (c / NB3) & 1);
+            tc::fence_after_sync();
+            if (F & F_MMA) {
+                const uint32_t b0 = wb + (c % NB3) * WST;
+                const uint32_t a0 = tm + 128 + (c % NA) * 64;
+                tc::mma12_3xtf32<2>(tm + 0, a0, tc::sdesc_sw128_lo(b0), tc::sdesc_sw128_lo(b0 + 8192), tc::idesc_tf32(128, 32));
+                tc::mma12_3xtf32<2>(tm + 64, a0, tc::sdesc_sw128_lo(b0 + 4096), tc::sdesc_sw128_lo(b0 + 12288), tc::idesc_tf32(128, 32));
+            }
+            tc::mma_commit_warp(&s.done[c % NBF]);
+            if (c % SEG == SEG - 1 || c == E - 1) { tc::mma_commit_warp(&s.seg_done); ++gs; }
+            __syncwarp();
+        }
+    } else if (warp == 1) {
+        if (lane == 0)
+            for (int c = 0; c < E; ++c) {
+                const int sv = c % NV3;
+                if (c >= NV3) tc::mbar_wait(&s.v_empty[sv], ((c / NV3) - 1) & 1);
+                tc::mbar_arrive_expect_tx(&s.v_full[sv], VST);
+                tc::bulk_g2s(&s.V[sv][0], vsrc + (cta_off + (size_t)c * VST) % vspan, VST, &s.v_full[sv]);
+            }
+    } else if (warp == 2) {
+        if (lane == 0)
+            for (int c = 0; c < E; ++c) {
+                const int sb = c % NB3;
+                if (c >= NB3) tc::mbar_wait(&s.done[(c - NB3) % NBF], ((c - NB3) / NBF) & 1);
+                tc::mbar_arrive_expect_tx(&s.b_full[sb], wbytes);
+                tc::bulk_g2s(&s.W[sb][0], wsrc + (cta_off / 4 + (size_t)(c % 64) * WST) % span, wbytes, &s.b_full[sb]);
+            }
+    } else if (warp == 3) {
+        const int nseg = (E + SEG - 1) / SEG;
+        float acc = 0.f;
+        for (int sg = 0; sg < nseg; ++sg) {
+            tc::mbar_wait(&s.seg_done, sg & 1);
+            tc::fence_after_sync();
+            for (int b = 0; b < 4; ++b) {     // lane quarter 3 only (one warp): enough to model the hand-off
+                uint32_t r[16];
+                tc::tmem_ld16(tm + ((uint32_t)(96) << 16) + (uint32_t)((b & 1) * 16 + (b >> 1) * 64), r);
+                tc::wait_ld();
+                for (int k = 0; k < 16; ++k) acc += __uint_as_float(r[k]);
+            }
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&s.seg_free);
+        }
+        if (__float_as_uint(acc) == 0x7fffffffu) out[2] = 3;
+    } else {
+        const int q4 = warp & 3, chl = q4 * 32 + lane;
+        uint32_t hi[32], lo[32];
+        float acc = 0.f;
+        for (int c = 0; c < E; ++c) {
+            const int sv = c % NV3;
+            tc::mbar_wait(&s.v_full[sv], (c / NV3) & 1);
+            const float* vs = reinterpret_cast<const float*>(&s.V[sv][0]) + chl;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) tc::split_tf32(vs[k * 128], hi[k], lo[k]);
+            float t = 0.f;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) t += __uint_as_float(lo[k]);
+            acc += t;
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&s.v_empty[sv]);
+            if (c >= NA) tc::mbar_wait(&s.done[(c - NA) % NBF], ((c - NA) / NBF) & 1);
+            tc::fence_after_sync();
+            const uint32_t ta = tm + ((uint32_t)(q4 * 32) << 16) + 128 + (c % NA) * 64;
+            tc::tmem_st32(ta, hi);
+            tc::tmem_st32(ta + 32, lo);
+            tc::wait_st();
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&s.a_full[c % NA]);
+        }
+        if (__float_as_uint(acc) == 0x7fffffffu) out[2] = 1;
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(&out[0], (unsigned long long)(clock64() - t0));
+    if (warp == 0) tc::tmem_dealloc(tm, tcols == 256 ? 256 : 512);
+}
+template <int F>
+void run3(const char* name, int per_sm, const uint8_t* v, const uint8_t* w, size_t span, unsigned long long* d,
+          size_t vspan, uint32_t wbytes = WST) {
+    const int E = 3000, grid = 148 * per_sm;
+    auto kern = k3<F>;
+    const int sm = sizeof(Smem3) + 1024;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    const int tcols = per_sm == 2 ? 256 : 512;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    kern<<<grid, 256, sm>>>(v, w, span, vspan, wbytes, E, tcols, d);
+    cudaMemset(d, 0, 24);
+    cudaEventRecord(e0);
+    kern<<<grid, 256, sm>>>(v, w, span, vspan, wbytes, E, tcols, d);
+    cudaEventRecord(e1);
+    cudaError_t e = cudaDeviceSynchronize();
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("k3 %-30s %d CTA/SM vspan %5zu MB: %7.1f cycles per entry per SM (events) %s\n", name, per_sm, vspan >> 20,
+           ms * 1e-3 * 1.965e9 / (E * per_sm), e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
 int main(int argc, char** argv) {
     const int only = argc > 1 ? atoi(argv[1]) : -1;
     int idx = 0;
@@ -384,10 +589,12 @@ int main(int argc, char** argv) {
     cudaMemset(w, 0, span + WST);
     cudaMalloc(&d, 64);
     constexpr int ALL = F_MMA | F_STTM | F_VLDS | F_VCP | F_WCP | F_PROMO;
-    const size_t S = 32u << 20;   // L2-resident value source
+    const size_t S = 32u << 20;
+    RUN((run3<F_MMA>("pipeline", 1, v, w, span, d, S)));
+    RUN((run3<F_MMA>("pipeline", 2, v, w, span, d, S)));
+    RUN((run3<F_MMA>("pipeline", 1, v, w, span, d, span)));
+    RUN((run3<F_MMA>("pipeline", 2, v, w, span, d, span)));
     RUN((run2<ALL, 6, 6, 2>("all", v, w, span, d, S)));
-    RUN((run2<F_MMA, 6, 6, 2>("MMA only", v, w, span, d, S)));
-    RUN((run2<ALL & ~F_MMA, 6, 6, 2>("all but MMA", v, w, span, d, S)));
-    RUN((run2<ALL & ~(F_VLDS | F_STTM), 6, 6, 2>("all but LDS/STTM", v, w, span, d, S)));
+    RUN((run2<ALL, 6, 6, 2>("all (V from HBM) w16K", v, w, span, d)));
     return 0;
 }
