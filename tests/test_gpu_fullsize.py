@@ -59,3 +59,34 @@ def test_fullsize_sampled_parity(name, channels, engine, monkeypatch):
     # whole-map sanity: no NaN on covered cells, W > 0 exactly where neighbours exist
     Wall = W.reshape(-1).cpu().numpy()
     assert info["n_pairs"] > 0 and (Wall > 0).sum() >= cov.sum()
+
+
+@pytest.mark.parametrize("kernel_v2", [False, True])
+def test_fullsize_zero_mean_scale_aware(kernel_v2, monkeypatch):
+    """cfg4 at full size in the bench's launch configuration with signed, zero-mean values
+    (the synthetic sky minus its 10 K baseline): the scale-aware rule of SURVEY.md 8(c) #11,
+    |V - V_ora| <= 1e-5 sum_n w |v_n| / W, on sampled cells x channels (the plain relative
+    rule is undefined where V ~ 0).  kernel_v2: the persistent kernel (HEGRID_TC_V2)."""
+    from parity_util import compare_scaled
+    if kernel_v2:
+        monkeypatch.setenv("HEGRID_TC_V2", "1")
+    w = synth.CONFIGS["cfg4"]
+    C = w.channels
+    lon, lat = synth.coords(w, device="cuda")
+    with Plan(lon, lat, w.map, w.fwhm_deg, engine="tc") as p:
+        perm = torch.as_tensor(p.permutation(), device="cuda")
+        vp = plan_layout_values(w, lon, lat, perm, list(range(C)))
+        vp -= 10.0
+        out = torch.empty((C, w.ny, w.nx), device="cuda")
+        W = torch.empty((w.ny, w.nx), device="cuda")
+        p.grid_plan_layout(vp, C, out, W)
+        torch.cuda.synchronize()
+        del vp
+    cells = sample_cells(w, k=60, seed=4)
+    chans = sample_channels(C, k=16)
+    vals = (synth.values(w, lon, lat, channels=torch.as_tensor(chans, device="cuda")) - 10.0).cpu().numpy()
+    g = out.reshape(C, -1)[torch.as_tensor(chans, device="cuda")][:, torch.as_tensor(cells, device="cuda")]
+    gw = W.reshape(-1)[torch.as_tensor(cells, device="cuda")]
+    st = compare_scaled(g.cpu().numpy(), gw.cpu().numpy(), lon.cpu().numpy(), lat.cpu().numpy(), vals,
+                        w.map, w.fwhm_deg, w.support, cells=cells)
+    assert st["covered"] > 0

@@ -121,11 +121,14 @@ def test_high_latitude_non_square_cells(engine, monkeypatch):
 
 def test_high_latitude_limit_is_refused():
     """Closer to the pole the pairs' half-longitude offsets exceed 0.5 rad, the fp32 series
-    distance's validated range: the lon/lat bin index refuses (EUNSUPPORTED)."""
+    distance's validated range: the lon/lat bin index refuses (EUNSUPPORTED) and AUTO builds
+    the HEALPix-indexed plan instead."""
     R = 1.0
     fwhm = R / 3.0 * 2.0 * math.sqrt(2.0 * math.log(2.0))
     m = dict(nx=10, ny=10, crval_lon=0.0, crval_lat=87.7, crpix_x=5.5, crpix_y=5.5,
              cdelt_lon=0.5, cdelt_lat=0.02)
     with pytest.raises(b.HegridError) as e:
-        Plan(np.array([0.0]), np.array([87.7]), m, fwhm)
+        Plan(np.array([0.0]), np.array([87.7]), m, fwhm, index="bins")
     assert e.value.code == 5
+    with Plan(np.array([0.0]), np.array([87.7]), m, fwhm) as p:      # AUTO: the HEALPix index
+        assert p.info()["index"] == 2

@@ -256,11 +256,22 @@ def test_domain_and_unsupported_errors():
         Plan(np.array([30.0]), np.array([91.0]), m, 0.05)
     assert e.value.code == 2
     with pytest.raises(b.HegridError) as e:
-        Plan(np.array([30.0]), np.array([41.0]), m, 1.0)        # R = 1.27 deg > 1 deg
+        Plan(np.array([30.0]), np.array([41.0]), m, 1.0, index="bins")        # R = 1.27 deg > 1 deg
     assert e.value.code == 5
     with pytest.raises(b.HegridError) as e:
-        Plan(np.array([30.0]), np.array([88.9]), mk_map(8, 8, 30, 88.9, 1 / 60), 0.05)
+        Plan(np.array([30.0]), np.array([88.9]), mk_map(8, 8, 30, 88.9, 1 / 60), 0.05, index="bins")
     assert e.value.code == 5
+    # AUTO serves both with the HEALPix index
+    for mm, fw in ((m, 1.0), (mk_map(8, 8, 30, 88.9, 1 / 60), 0.05)):
+        with Plan(np.array([30.0]), np.array([41.0 if fw == 1.0 else 88.9]), mm, fw) as p:
+            assert p.info()["index"] == 2
+    # domain errors are domain errors for the HEALPix index too
+    with pytest.raises(b.HegridError) as e:
+        Plan(np.array([30.0]), np.array([91.0]), m, 0.05, index="healpix")
+    assert e.value.code == 2
+    with pytest.raises(b.HegridError) as e:
+        Plan(np.array([30.0]), np.array([41.0]), m, 0.05, index="nosuch")
+    assert False, "unknown index must raise
 
 
 def test_device_coordinate_plan_matches_host_plan():
