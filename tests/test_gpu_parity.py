@@ -269,9 +269,10 @@ def test_domain_and_unsupported_errors():
     with pytest.raises(b.HegridError) as e:
         Plan(np.array([30.0]), np.array([91.0]), m, 0.05, index="healpix")
     assert e.value.code == 2
+    opts = b.make_opts(index=7)
     with pytest.raises(b.HegridError) as e:
-        Plan(np.array([30.0]), np.array([41.0]), m, 0.05, index="nosuch")
-    assert False, "unknown index must raise
+        b.hegrid_plan_create(np.array([30.0]), np.array([41.0]), m, 0.05, 3.0, opts)
+    assert e.value.code == 1
 
 
 def test_device_coordinate_plan_matches_host_plan():
