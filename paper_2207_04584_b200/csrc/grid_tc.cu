@@ -31,7 +31,7 @@
 //                     tensor core's truncating accumulation);
 //   B producers (OTF): compute the chunk's weights into 2 shared weight stages.
 // Epilogue: the last segments are promoted, V = S / W (IEEE div), NaN where W = 0, written as
-// coalesced row segments.  The persistent variant k_accum_pw is described further down.
+// coalesced row segments.
 // Deterministic: fixed chunk order, fixed work mapping, no atomics.
 #include <stdio.h>
 #include <stdlib.h>
@@ -1261,478 +1261,6 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     if (warp == 0) tc::tmem_dealloc(tmem, TMEM_COLS);
 }
 
-// ================================================================== persistent PW kernel
-// k_accum_pw: the precomputed-weight mode as a persistent kernel (one CTA per SM walking a
-// static list of work items = (tile, entry part, 128-channel block)), with the pipeline
-// roles decoupled so that no role waits on another's side work:
-//   warp 0      : MMA issuer (all block rows; 12 MMAs per run of in-reach blocks)
-//   warp 1      : value loader: one 2D TMA box per entry into a PW_NV-stage ring
-//   warp 2      : weight loader: the entry's image bytes into a byte ring (PW_RING)
-//   warps 4-7   : A producers: thread = channel = TMEM lane, 32 samples per entry: split
-//                 into tf32 hi / lo and tcgen05.st into one of 2 TMEM A stages
-//   warps 8-19  : promoters: the fp32 master sums live in their registers (group g = warps
-//                 8 + 4g .. 11 + 4g owns blocks 4g .. 4g + 3, 64 cells per channel); they add
-//                 each finished D segment into them (round-to-nearest), re-zero it, and write
-//                 the work item's V = S / W after its last segment.
-// The accumulation order per (cell, channel) is the chunk order of the schedule in segments
-// of SEG entries, exactly as k_accum_tc<SEG, true>, so the maps are bit-identical.
-constexpr int PW_NV = 5;
-constexpr uint32_t PW_RING = 104 * 1024;
-constexpr int PW_STG_LD = 17;              // epilogue staging row (16 cells + 1: conflict-free writes)
-constexpr int PW_NA = 5;                   // TMEM A stages (64 columns each, after the D tile)
-constexpr uint32_t PW_A_COL0 = D_COLS;     // single D tile at columns [0, 192)
-static_assert(PW_A_COL0 + PW_NA * 2 * TC_KC <= TMEM_COLS, "TMEM budget");
-constexpr int PW_NPG = 3;                  // promoter groups (4 warps each)
-constexpr int PW_BPG = TC_NB / PW_NPG;     // blocks per promoter group
-static_assert(TC_NB % PW_NPG == 0, "promoter groups");
-constexpr int PW_NI = TC_BY;               // MMA issuer warps: issuer i issues block row i
-constexpr int PW_THREADS = 32 * (8 + 4 * PW_NPG);
-static_assert(PW_NI == 3, "issuers on warps 0, 2, 3");
-struct PwSmem {
-    uint8_t ring[PW_RING];
-    uint8_t Vs[PW_NV][V_STAGE];
-    uint4 Es[PW_NV];
-    uint32_t Bmask[NBF], Boff[NBF];
-    long long Wstart[NBF];                 // weight loader: ring position of each in-flight entry
-    uint64_t a_full[PW_NA], b_full[NBF], done[NBF], v_full[PW_NV], v_empty[PW_NV];
-    uint64_t seg_done, seg_free;
-    uint32_t tmem_base;
-    uint32_t sink[PW_THREADS];             // dependency sink, one word per thread
-    float stage[4 * PW_NPG][32][PW_STG_LD];   // epilogue staging, one tile per promoter warp
-};
-static_assert(sizeof(PwSmem) + 1024 <= 232448, "shared memory budget");
-static_assert(offsetof(PwSmem, Vs) % 1024 == 0, "stage alignment");
-
-struct PwItem {
-    int tile, cblk, sp;
-    uint32_t e0, n;        // first schedule entry (global index), number of entries
-};
-// item -> (tile, part, channel block): the channel blocks of a tile part are adjacent, so the
-// CTAs working on them at the same time share the part's weight entries in L2
-__device__ __forceinline__ PwItem pw_item(int it, const uint32_t* __restrict__ tile_off, int ncb,
-                                          int nsplit) {
-    PwItem I;
-    I.cblk = it % ncb;
-    const int r = it / ncb;
-    I.sp = r % nsplit;
-    I.tile = r / nsplit;
-    const uint32_t t0 = __ldg(&tile_off[I.tile]), all = __ldg(&tile_off[I.tile + 1]) - t0;
-    const uint32_t eb = (uint32_t)((uint64_t)all * I.sp / nsplit);
-    I.e0 = t0 + eb;
-    I.n = (uint32_t)((uint64_t)all * (I.sp + 1) / nsplit) - eb;
-    return I;
-}
-
-// HG_PW_PROF builds: per-role cycle counters (summed over CTAs) in g_tc_prof, printed by the
-// launcher with HEGRID_TC_DEBUG=32
-#ifdef HG_PW_PROF
-__device__ long long g_pw_tl[64][12];
-#define PTL(ev) do { if (blockIdx.x == 7 && lane == 0 && gc >= 300 && gc < 364) g_pw_tl[gc - 300][ev] = clock64(); } while (0)
-#define PWP(k, ...) do { const long long _t = clock64(); __VA_ARGS__; if (lane == 0) pwc[k] += clock64() - _t; } while (0)
-#else
-#define PWP(k, ...) do { __VA_ARGS__; } while (0)
-#define PTL(ev) do { } while (0)
-#endif
-template <int SEG>
-__global__ void __launch_bounds__(PW_THREADS, 1)
-k_accum_pw(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap tmap_v,
-           const uint4* __restrict__ sched, const uint32_t* __restrict__ tile_off,
-           const float* __restrict__ wsum, const uint8_t* __restrict__ wimg,
-           const uint32_t* __restrict__ wslot, int C, int ncb, int nsplit, int n_items,
-           float* __restrict__ part, float* __restrict__ out, float* __restrict__ wout, NfBuf nf) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    PwSmem& sm = *reinterpret_cast<PwSmem*>(smem_raw);
-    if (tc::smem_u32(smem_raw) & 1023u) __trap();
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int tiles_x = (g.nx + TC_TW - 1) / TC_TW;
-    const int64_t cells = (int64_t)g.nx * g.ny;
-    constexpr int NAW = 4, NPW = 4 * PW_NPG;
-#ifdef HG_PW_PROF
-    long long pwc[16] = {0};
-    const long long t_begin = clock64();
-#endif
-
-    if (warp == 0) tc::tmem_alloc(&sm.tmem_base, TMEM_COLS);
-    if (tid == 32) {
-        for (int s = 0; s < PW_NA; ++s) tc::mbar_init(&sm.a_full[s], NAW);
-        for (int s = 0; s < NBF; ++s) {
-            tc::mbar_init(&sm.done[s], PW_NI);       // one commit per issuer
-            tc::mbar_init(&sm.b_full[s], 1);
-        }
-        for (int s = 0; s < PW_NV; ++s) {
-            tc::mbar_init(&sm.v_full[s], 1);
-            tc::mbar_init(&sm.v_empty[s], NAW);
-        }
-        tc::mbar_init(&sm.seg_done, PW_NI);
-        tc::mbar_init(&sm.seg_free, NPW);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    const uint32_t tmem = sm.tmem_base;
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-
-    const int issuer = warp == 0 ? 0 : warp == 2 ? 1 : warp == 3 ? 2 : -1;
-    if (issuer >= 0) {
-        // ================================ MMA issuers ===============================
-        // issuer i issues the MMAs of block row i (each D block is always fed by the same
-        // issuer in entry order, so the accumulation order is fixed); three instruction
-        // streams share the per-MMA issue cost (operand conversion to uniform registers)
-        // One D tile (single-buffered): a segment's first MMA into a block overwrites it
-        // (accumulate flag 0, `touched`), so D needs no zeroing; before segment s + 1 starts,
-        // the promoters must have read segment s out of it (seg_free).
-        uint32_t gc = 0, gs = 0;
-        const uint32_t rows = 0xFu << (TC_BX * issuer);
-        for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-            const PwItem I = pw_item(it, tile_off, ncb, nsplit);
-            uint32_t touched = 0;
-            for (uint32_t c = 0; c < I.n; ++c, ++gc) {
-                if (c % SEG == 0) {
-                    touched = 0;
-                    if (gs >= 1) {
-                        PWP(3, tc::mbar_wait(&sm.seg_free, (gs - 1) & 1));
-                        tc::fence_after_sync();
-                    }
-                }
-                const uint32_t sa = gc % PW_NA, k = gc % NBF;
-                PWP(1, tc::mbar_wait(&sm.a_full[sa], (gc / PW_NA) & 1));
-                PTL(0);
-                PWP(2, tc::mbar_wait(&sm.b_full[k], (gc / NBF) & 1));
-                PTL(1);
-                tc::fence_after_sync();
-#ifdef HG_PW_PROF
-                const long long t_iss = clock64();
-#endif
-                const uint32_t mask = sm.Bmask[k];
-                const uint32_t b_addr = tc::smem_u32(&sm.ring[sm.Boff[k]]);
-                const int ns = __popc(mask);
-                const uint32_t lo16 = (uint32_t)((ns * SLOT_BYTES) >> 4);
-                const uint32_t dh0 = tc::sdesc_sw128_lo(b_addr);
-                const uint32_t a0 = tmem + PW_A_COL0 + sa * 2 * TC_KC;
-                uint32_t mm = mask & rows;
-                while (mm) {
-                    // a run of consecutive in-reach blocks, cut where the first-touch state changes
-                    const int b = __ffs(mm) - 1;
-                    const uint32_t t = (touched >> b) & 1u;
-                    const uint32_t same = t ? touched : ~touched;
-                    const int r = __ffs(~((mm & same) >> b)) - 1;
-                    const uint32_t run = ((1u << r) - 1u) << b;
-                    mm &= ~run;
-                    touched |= run;
-                    const int q = __popc(mask & ((1u << b) - 1u));
-                    static_assert(KA == 1, "32-sample chunks");
-                    const uint32_t bh = dh0 + (uint32_t)((q * ATOM_SLOT) >> 4);
-                    tc::mma12_3xtf32_acc<(32 >> 4), TC_KC>(tmem + (uint32_t)(b * TC_N), a0, bh, bh + lo16,
-                                                           tc::idesc_tf32(TC_M, TC_N * r), t);
-                }
-                tc::mma_commit_warp(&sm.done[k]);
-#ifdef HG_PW_PROF
-                if (lane == 0) pwc[4] += clock64() - t_iss;
-#endif
-                PTL(2);
-                if (c % SEG == SEG - 1 || c == I.n - 1) {
-                    tc::mma_commit_warp(&sm.seg_done);
-                    ++gs;
-                }
-                __syncwarp();
-            }
-        }
-    } else if (warp == 1) {
-        // ================================ loader ====================================
-        // one lane, per entry: the value tile (one 2D TMA box into a PW_NV-stage ring) and the
-        // entry's weight image bytes (nq x 4 KB, one bulk copy into a byte ring at the next
-        // contiguous offset, wrapping to 0; bytes are reused once every entry placed there
-        // has completed: done[] phases, confirmed in order; at most NBF entries in flight).
-        // Entries are read G at a time into registers (static indices), two groups ahead, so
-        // no global-load latency sits on the loop; no warp collectives (a shuffle after a
-        // single-lane section takes the divergent slow path).
-        if (lane == 0) {
-            constexpr int G = 4, PF = PW_NV + 3;
-            static_assert(PF <= 2 * G, "prefetch distance within the loaded groups");
-            uint32_t gc = 0, conf = 0;
-            long long head = 0;
-            for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-                const PwItem I = pw_item(it, tile_off, ncb, nsplit);
-                const int cb = I.cblk * TC_M;
-                const uint4* es = sched + I.e0;
-                const uint32_t* ws = wslot + I.e0;
-                uint4 e0[G], e1[G], e2[G];          // {x, y, z, weight slot}
-                auto ldg = [&](uint32_t c0, uint4 (&e)[G]) {
-#pragma unroll
-                    for (int u = 0; u < G; ++u) {
-                        if (c0 + u < I.n) {
-                            const uint4 t = __ldg(&es[c0 + u]);
-                            e[u] = make_uint4(t.x, t.y, t.z, __ldg(&ws[c0 + u]));
-                        } else {
-                            e[u] = make_uint4(0, 0, 0, 0);
-                        }
-                    }
-                };
-                ldg(0, e0);
-                ldg(G, e1);
-                ldg(2 * G, e2);
-                for (uint32_t c = 0; c < PF && c < I.n; ++c) tc::tma_prefetch_2d(&tmap_v, cb, (int)__ldg(&es[c].x));
-                for (uint32_t c0 = 0; c0 < I.n; c0 += G) {
-#pragma unroll
-                    for (int u = 0; u < G; ++u) {
-                        const uint32_t c = c0 + u;
-                        if (c >= I.n) break;
-                        const uint4 e = e0[u];
-#ifndef HG_PW_NOPF
-                        // L2 prefetch of the value tile PF entries ahead
-                        const uint32_t xp = u + PF - G < G ? e1[(u + PF - G) % G].x : e2[(u + PF - 2 * G) % G].x;
-                        if (c + PF < I.n) tc::tma_prefetch_2d(&tmap_v, cb, (int)xp);
-#endif
-                        // ---- value tile
-                        const int sv = gc % PW_NV;
-                        if (gc >= PW_NV) PWP(5, tc::mbar_wait(&sm.v_empty[sv], ((gc / PW_NV) - 1) & 1));
-                        sm.Es[sv] = make_uint4(e.x, e.y, e.z, 0u);
-#ifdef HG_PW_NOV
-                        tc::mbar_arrive(&sm.v_full[sv]);
-#else
-                        tc::mbar_arrive_expect_tx(&sm.v_full[sv], (uint32_t)V_STAGE);
-                        tc::tma_load_2d(&sm.Vs[sv][0], &tmap_v, cb, (int)e.x, &sm.v_full[sv]);
-#endif
-                        PTL(4);
-                        // ---- weight bytes
-#ifdef HG_TC_HALFW
-                        const uint32_t bytes = __popc(e.z) * 1u * SLOT_BYTES;   // timing experiment
-#else
-                        const uint32_t bytes = __popc(e.z) * 2u * SLOT_BYTES;
-#endif
-                        long long off = head % PW_RING;
-                        if (off + bytes > PW_RING) {
-                            head += PW_RING - off;
-                            off = 0;
-                        }
-#ifdef HG_PW_NORINGWAIT
-                        while (conf + NBF <= gc) {
-#else
-                        while (conf < gc && (gc - conf >= NBF || sm.Wstart[conf % NBF] < head + (long long)bytes - PW_RING)) {
-#endif
-                            PWP(6, tc::mbar_wait(&sm.done[conf % NBF], (conf / NBF) & 1));
-                            ++conf;
-                        }
-                        const uint32_t k = gc % NBF;
-                        sm.Wstart[k] = head;
-                        sm.Bmask[k] = e.z;
-                        sm.Boff[k] = (uint32_t)off;
-                        tc::mbar_arrive_expect_tx(&sm.b_full[k], bytes);
-                        tc::bulk_g2s(&sm.ring[off], wimg + (size_t)e.w * (2u * SLOT_BYTES), bytes, &sm.b_full[k]);
-                        PTL(3);
-                        head += bytes;
-                        ++gc;
-                    }
-#pragma unroll
-                    for (int u = 0; u < G; ++u) {
-                        e0[u] = e1[u];
-                        e1[u] = e2[u];
-                    }
-                    ldg(c0 + 3 * G, e2);
-                }
-            }
-        }
-    } else if (warp >= 4 && warp < 8) {
-        // ================================ A producers ===============================
-        const int q4 = warp & 3, chl = q4 * 32 + lane;
-        uint32_t gc = 0;
-        for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-            const PwItem I = pw_item(it, tile_off, ncb, nsplit);
-            const int cb = I.cblk * TC_M;
-            for (uint32_t c = 0; c < I.n; ++c, ++gc) {
-                const int sv = gc % PW_NV;
-                PWP(7, tc::mbar_wait(&sm.v_full[sv], (gc / PW_NV) & 1));
-                if (warp == 4) PTL(5);
-#ifdef HG_PW_PROF
-                const long long t_a = clock64();
-#endif
-                const uint4 ee = sm.Es[sv];
-                const uint32_t nk = ee.y & 255;
-                const float* vs = reinterpret_cast<const float*>(&sm.Vs[sv][0]) + chl;
-                // the raw values (rows >= nk belong to other entries: 0)
-                uint32_t v[TC_KC];
-#ifdef HG_PW_NOLDS
-#pragma unroll
-                for (int k = 0; k < TC_KC; ++k) v[k] = ee.x + k * 77;
-#else
-                if (nk == TC_KC) {
-#pragma unroll
-                    for (int k = 0; k < TC_KC; ++k) v[k] = __float_as_uint(vs[k * TC_M]);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < TC_KC; ++k) v[k] = (uint32_t)k < nk ? __float_as_uint(vs[k * TC_M]) : 0u;
-                }
-#endif
-                // largest magnitude bit pattern: >= kNfBits iff some value is NaN / Inf or
-                // would round to Inf in tf32 (tc::split_tf32's hi)
-                uint32_t mx = 0;
-#pragma unroll
-                for (int k = 0; k < TC_KC; ++k) mx = max(mx, v[k] & 0x7FFFFFFFu);
-                // release the value stage only after every loaded word was consumed (an
-                // mbarrier arrive does not wait for outstanding shared loads): store a value
-                // that depends on all of them first
-                asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[tid])), "r"(ee.x ^ mx) : "memory");
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&sm.v_empty[sv]);
-                // non-finite values: zeroed here, applied by the fix-up (nonfinite.cuh)
-                constexpr uint32_t kNfBits = 0x7F7FF000u;
-                if (mx >= kNfBits) {
-#pragma unroll
-                    for (int k = 0; k < TC_KC; ++k) {
-                        if ((v[k] & 0x7FFFFFFFu) < kNfBits) continue;
-                        v[k] = 0u;
-                        if ((uint32_t)k < nk && cb + chl < C) nf_record(nf, ee.x + k, cb + chl);
-                    }
-                }
-#ifdef HG_PW_PROF
-                if (lane == 0) pwc[9] += clock64() - t_a;
-#endif
-                if (gc >= PW_NA) PWP(8, tc::mbar_wait(&sm.done[(gc - PW_NA) % NBF], ((gc - PW_NA) / NBF) & 1));
-                if (warp == 4) PTL(6);
-                tc::fence_after_sync();
-                const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + PW_A_COL0 + (gc % PW_NA) * 2 * TC_KC;
-#ifndef HG_PW_NOSTTM
-                // split x = hi + lo (tc::split_tf32) in two halves of 16: lo to TMEM, hi in place
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    uint32_t lo[16];
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        uint32_t hk;
-                        tc::split_tf32(__uint_as_float(v[16 * h + k]), hk, lo[k]);
-                        v[16 * h + k] = hk;
-                    }
-                    tc::tmem_st16(ta + TC_KC + 16 * h, lo);
-                }
-                tc::tmem_st32(ta, v);
-                PWP(10, tc::wait_st());
-#else
-                (void)ta;
-#endif
-                tc::fence_before_sync();
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&sm.a_full[gc % PW_NA]);
-                if (warp == 4) PTL(7);
-            }
-        }
-    } else if (warp >= 8) {
-        // ================================ promoters =================================
-        const int q4 = warp & 3, grp = (warp - 8) >> 2, chl = q4 * 32 + lane;
-        const uint32_t trow = tmem + ((uint32_t)(q4 * 32) << 16);
-        const float qnan = __int_as_float(0x7fc00000);
-        float m[PW_BPG * TC_N];
-#pragma unroll
-        for (int k = 0; k < PW_BPG * TC_N; ++k) m[k] = 0.0f;
-        uint32_t gs = 0;
-        for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-            const PwItem I = pw_item(it, tile_off, ncb, nsplit);
-            const uint32_t nseg = (I.n + SEG - 1) / SEG;
-            for (uint32_t s = 0; s < nseg; ++s, ++gs) {
-                uint32_t mask = 0;
-                const uint32_t c1 = min(I.n, (s + 1) * SEG);
-                for (uint32_t c = s * SEG; c < c1; ++c) mask |= __ldg(&sched[I.e0 + c].z);
-                // one warp waits on the segment's completion (low wake-up latency), the other
-                // promoter warps park on a named barrier (no issue slots while waiting)
-                if (warp == 8) PWP(11, tc::mbar_wait(&sm.seg_done, gs & 1));
-                asm volatile("bar.sync 1, %0;" :: "n"(32 * NPW) : "memory");
-                tc::fence_after_sync();
-#ifdef HG_PW_PROF
-                const long long t_p = clock64();
-#endif
-                // add the segment's blocks of this group into the master sums, then free D for
-                // the next segment (whose first touches overwrite it)
-#pragma unroll
-                for (int bl = 0; bl < PW_BPG; ++bl) {
-                    const int b = grp * PW_BPG + bl;
-                    if ((mask >> b) & 1u) {
-                        uint32_t r[16];
-                        tc::tmem_ld16(trow + (uint32_t)(b * TC_N), r);
-                        tc::wait_ld();
-#pragma unroll
-                        for (int k = 0; k < 16; ++k) m[bl * 16 + k] += __uint_as_float(r[k]);
-                    }
-                }
-                tc::fence_before_sync();
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&sm.seg_free);
-#ifdef HG_PW_PROF
-                if (lane == 0) pwc[12] += clock64() - t_p;
-#endif
-            }
-#ifdef HG_PW_PROF
-            const long long t_e = clock64();
-#endif
-            // ---- the item's V = S / W (Eq. 1's division), NaN where W = 0.  Group g holds
-            // block row g (16 x 4 cells) of its 32 channels; each cell row goes through a
-            // per-warp staging tile so that a store instruction writes two channels' 64-byte
-            // row segments (instead of 32 scattered words)
-            static_assert(PW_BPG == TC_BX, "a promoter group owns one block row");
-            const int i0 = (I.tile % tiles_x) * TC_TW, j0 = (I.tile / tiles_x) * TC_TH;
-            float* stg = &sm.stage[warp - 8][0][0];
-            const int xo = lane & 15, chp = lane >> 4;
-            const bool x_ok = i0 + xo < g.nx;
-#ifndef HG_PW_NOEPI
-#pragma unroll
-            for (int cy = 0; cy < 4; ++cy) {
-                const int j = j0 + grp * 4 + cy;
-                if (j >= g.ny) break;
-                const int64_t rowc = (int64_t)j * g.nx + i0;
-#pragma unroll
-                for (int bl = 0; bl < PW_BPG; ++bl)
-#pragma unroll
-                    for (int cx = 0; cx < 4; ++cx) {
-                        const float S = m[bl * 16 + cy * 4 + cx];
-                        float V = S;
-                        if (nsplit == 1) {
-                            const int x = bl * 4 + cx;
-                            const float W = i0 + x < g.nx ? __ldg(&wsum[rowc + x]) : 0.0f;
-                            V = W > 0.0f ? __fdiv_rn(S, W) : qnan;
-                        }
-                        stg[lane * PW_STG_LD + bl * 4 + cx] = V;
-                    }
-                __syncwarp();
-#pragma unroll 4
-                for (int r = 0; r < 16; ++r) {
-                    const int cl = 2 * r + chp;                      // channel within the warp
-                    const int ch = I.cblk * TC_M + q4 * 32 + cl;
-                    const float V = stg[cl * PW_STG_LD + xo];
-                    if (ch < C && x_ok) {
-                        if (nsplit > 1) part[((int64_t)I.sp * C + ch) * cells + rowc + xo] = V;
-                        else out[(int64_t)ch * cells + rowc + xo] = V;
-                    }
-                }
-                __syncwarp();
-            }
-#endif
-#pragma unroll
-            for (int k = 0; k < PW_BPG * TC_N; ++k) m[k] = 0.0f;
-#ifdef HG_PW_PROF
-            if (lane == 0) pwc[13] += clock64() - t_e;
-#endif
-            if (wout != nullptr && I.cblk == 0 && I.sp == 0) {
-                const int t = tid - 8 * 32;            // 0 .. 32 NPW - 1
-                if (t < TC_TW * TC_TH && t < 32 * NPW) {
-                    const int i = i0 + t % TC_TW, j = j0 + t / TC_TW;
-                    if (i < g.nx && j < g.ny) wout[(int64_t)j * g.nx + i] = __ldg(&wsum[(int64_t)j * g.nx + i]);
-                }
-            }
-        }
-    }
-#ifdef HG_PW_PROF
-    if (lane == 0 && (warp == 0 || warp == 1 || warp == 4 || warp == 8)) {
-        if (warp == 0) atomicAdd(&g_tc_prof[0], (unsigned long long)(clock64() - t_begin));
-        for (int q = 1; q < 16; ++q)
-            if (pwc[q]) atomicAdd(&g_tc_prof[q], (unsigned long long)pwc[q]);
-    }
-#endif
-    tc::fence_before_sync();
-    __syncthreads();
-    if (warp == 0) tc::tmem_dealloc(tmem, TMEM_COLS);
-}
-
 // Split tiles: out = (sum of the parts' partial sums, in part order) / W, NaN where W = 0.
 __global__ void k_tc_reduce(const float* __restrict__ part, int nsplit, int64_t n, int64_t cells,
                             const float* __restrict__ wsum, float* __restrict__ out) {
@@ -1818,52 +1346,13 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     if (const char* e = getenv("HEGRID_TC_SNAKE")) snake = atoi(e);
     NfBuf nf;
     HG_TRY_S(nonfinite_alloc(p, &nf, st));
-    // the persistent kernel (k_accum_pw) is opt-in while it is slower than the round-1 kernel
-    static const bool v1 = getenv("HEGRID_TC_V2") == nullptr;
-    if (pw && !v1) {
-        // persistent: one CTA per SM over the work items (tile, part, channel block)
-        int nsm = 148, dev = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        const int n_items = tiles * nsplit * ncb;
-        auto kp = sparse ? k_accum_pw<SEG_SPARSE> : k_accum_pw<SEG_DENSE>;
-        const size_t psm = sizeof(PwSmem);
-        HG_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
-        kp<<<std::min(n_items, nsm), PW_THREADS, psm, st>>>(g, tmap, p->d_tc_sched, p->d_tc_tile_off,
-                                                            p->d_tc_wsum, p->d_tc_wimg, p->d_tc_wslot, C,
-                                                            ncb, nsplit, n_items, d_part, d_out, d_weight, nf);
-        count_launch();
-#ifdef HG_PW_PROF
-        if (dbg & 32) {
-            unsigned long long h[16];
-            cudaStreamSynchronize(st);
-            cudaMemcpyFromSymbol(h, g_tc_prof, sizeof(h));
-            const double ctas = std::min(n_items, nsm), tot = (double)h[0];
-            fprintf(stderr, "[pw prof] cycles/CTA %.0f | issuer: waitA %.3f waitB %.3f waitSegFree %.3f issue %.3f | "
-                    "L waitVEmpty %.3f waitRing %.3f | A: waitV %.3f work %.3f waitDone %.3f sttm %.3f | "
-                    "P: waitSeg %.3f promote %.3f epilogue %.3f (fractions of CTA time, per warp)\n",
-                    tot / ctas, h[1] / tot, h[2] / tot, h[3] / tot, h[4] / tot, h[5] / tot, h[6] / tot, h[7] / tot,
-                    h[9] / tot, h[8] / tot, h[10] / tot, h[11] / tot, h[12] / tot, h[13] / tot);
-            unsigned long long z[16] = {0};
-            cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
-            static long long tl[64][12];
-            cudaMemcpyFromSymbol(tl, g_pw_tl, sizeof(tl));
-            fprintf(stderr, "[pw tl] entry: Wtop Wshfl Wring Wcopy Vtma | Avfull Adone Aafull | IgotA IgotB Iissued (cycles rel. to entry 0 IgotA)\n");
-            for (int c = 0; c < 64; ++c)
-                fprintf(stderr, "[pw tl] %3d: %8lld %8lld %8lld %8lld %8lld | %8lld %8lld %8lld | %8lld %8lld %8lld\n", c,
-                        tl[c][8] - tl[0][0], tl[c][9] - tl[0][0], tl[c][10] - tl[0][0], tl[c][3] - tl[0][0],
-                        tl[c][4] - tl[0][0], tl[c][5] - tl[0][0], tl[c][6] - tl[0][0], tl[c][7] - tl[0][0],
-                        tl[c][0] - tl[0][0], tl[c][1] - tl[0][0], tl[c][2] - tl[0][0]);
-        }
-#endif
-    } else {
-        auto kern = pw ? (sparse ? k_accum_tc<SEG_SPARSE, true> : k_accum_tc<SEG_DENSE, true>)
-                       : (sparse ? k_accum_tc<SEG_SPARSE, false> : k_accum_tc<SEG_DENSE, false>);
-        HG_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched, p->d_tc_tile_off,
-                                             p->d_tc_wsum, p->d_tc_wimg, p->d_tc_wslot, C, tiles, cgroup,
-                                             super_, snake, nsplit, d_part, d_out, d_weight, nf, dbg);
-        count_launch();
-    }
+    auto kern = pw ? (sparse ? k_accum_tc<SEG_SPARSE, true> : k_accum_tc<SEG_DENSE, true>)
+                   : (sparse ? k_accum_tc<SEG_SPARSE, false> : k_accum_tc<SEG_DENSE, false>);
+    HG_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, TC_THREADS, smem, st>>>(g, tmap, p->dev(), p->d_tc_sched, p->d_tc_tile_off,
+                                         p->d_tc_wsum, p->d_tc_wimg, p->d_tc_wslot, C, tiles, cgroup,
+                                         super_, snake, nsplit, d_part, d_out, d_weight, nf, dbg);
+    count_launch();
     if (nsplit > 1) {
         const int64_t n = (int64_t)C * g.nx * g.ny;
         k_tc_reduce<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(

@@ -156,45 +156,6 @@ __device__ __forceinline__ void mma12_3xtf32(uint32_t d, uint32_t a0, uint32_t b
         "n"(ALO + 16), "n"(ALO + 24) : "memory");
 #undef HG_MMA12_KS
 }
-// mma12_3xtf32 with the accumulate flag of the first MMA as an operand: acc0 == 0 overwrites
-// D with the run's first product (a D block's first touch in a segment), so D needs no zeroing.
-template <int KS_STEP, int ALO = 32>
-__device__ __forceinline__ void mma12_3xtf32_acc(uint32_t d, uint32_t a0, uint32_t bh_lo, uint32_t bl_lo,
-                                                 uint32_t idesc, uint32_t acc0) {
-#define HG_MMA12A_KS(bh, bl, ah, al)                                                     \
-    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+" #ah "], " #bh ", %4, 1;\n\t"       \
-    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+" #ah "], " #bl ", %4, 1;\n\t"       \
-    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+" #al "], " #bh ", %4, 1;\n\t"
-    asm volatile(
-        "{\n\t"
-        ".reg .pred e, p;\n\t"
-        ".reg .b32 x1, x2, x3, y1, y2, y3;\n\t"
-        ".reg .b64 h0, h1, h2, h3, l0, l1, l2, l3;\n\t"
-        "add.u32 x1, %2, %5;\n\t"
-        "add.u32 x2, %2, %6;\n\t"
-        "add.u32 x3, %2, %7;\n\t"
-        "add.u32 y1, %3, %5;\n\t"
-        "add.u32 y2, %3, %6;\n\t"
-        "add.u32 y3, %3, %7;\n\t"
-        "mov.b64 h0, {%2, %8};\n\t"
-        "mov.b64 h1, {x1, %8};\n\t"
-        "mov.b64 h2, {x2, %8};\n\t"
-        "mov.b64 h3, {x3, %8};\n\t"
-        "mov.b64 l0, {%3, %8};\n\t"
-        "mov.b64 l1, {y1, %8};\n\t"
-        "mov.b64 l2, {y2, %8};\n\t"
-        "mov.b64 l3, {y3, %8};\n\t"
-        "setp.ne.b32 p, %13, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], h0, %4, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], l0, %4, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+%9], h0, %4, 1;\n\t"
-        HG_MMA12A_KS(h1, l1, 8, %10) HG_MMA12A_KS(h2, l2, 16, %11) HG_MMA12A_KS(h3, l3, 24, %12)
-        "}\n" :: "r"(d), "r"(a0), "r"(bh_lo), "r"(bl_lo), "r"(idesc), "n"(KS_STEP),
-        "n"(2 * KS_STEP), "n"(3 * KS_STEP), "n"(kDescHiSw128), "n"(ALO), "n"(ALO + 8),
-        "n"(ALO + 16), "n"(ALO + 24), "r"(acc0) : "memory");
-#undef HG_MMA12A_KS
-}
 // low word of a K-major SWIZZLE_128B descriptor (start address >> 4, LBO field 1)
 __device__ __forceinline__ uint32_t sdesc_sw128_lo(uint32_t saddr) {
     return ((saddr >> 4) & 0x3FFFu) | (1u << 16);

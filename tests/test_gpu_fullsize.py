@@ -61,15 +61,12 @@ def test_fullsize_sampled_parity(name, channels, engine, monkeypatch):
     assert info["n_pairs"] > 0 and (Wall > 0).sum() >= cov.sum()
 
 
-@pytest.mark.parametrize("kernel_v2", [False, True])
-def test_fullsize_zero_mean_scale_aware(kernel_v2, monkeypatch):
+def test_fullsize_zero_mean_scale_aware():
     """cfg4 at full size in the bench's launch configuration with signed, zero-mean values
     (the synthetic sky minus its 10 K baseline): the scale-aware rule of SURVEY.md 8(c) #11,
     |V - V_ora| <= 1e-5 sum_n w |v_n| / W, on sampled cells x channels (the plain relative
-    rule is undefined where V ~ 0).  kernel_v2: the persistent kernel (HEGRID_TC_V2)."""
+    rule is undefined where V ~ 0)."""
     from parity_util import compare_scaled
-    if kernel_v2:
-        monkeypatch.setenv("HEGRID_TC_V2", "1")
     w = synth.CONFIGS["cfg4"]
     C = w.channels
     lon, lat = synth.coords(w, device="cuda")

@@ -20,7 +20,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
-MODES = ["simt", "tc_otf", "tc_pw", "tc_v2"]
+MODES = ["simt", "tc_otf", "tc_pw"]
 
 
 def _run(tool, mode):

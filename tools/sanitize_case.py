@@ -1,5 +1,5 @@
 """A small gridding run through the C-ABI without torch (numpy inputs, host API), for
-compute-sanitizer: python tools/sanitize_case.py <simt|tc_otf|tc_pw|tc_v2>."""
+compute-sanitizer: python tools/sanitize_case.py <simt|tc_otf|tc_pw>."""
 import os
 import sys
 
@@ -12,10 +12,8 @@ mode = sys.argv[1]
 engine = "simt" if mode == "simt" else "tc"
 if mode == "tc_otf":
     os.environ["HEGRID_TC_PW"] = "0"
-elif mode in ("tc_pw", "tc_v2"):
+elif mode == "tc_pw":
     os.environ["HEGRID_TC_PW"] = "1"
-if mode == "tc_v2":
-    os.environ["HEGRID_TC_V2"] = "1"
 rng = np.random.default_rng(2207)
 for n, C, nx, ny, fw in ((5000, 1, 64, 64, 3 / 60), (3000, 133, 21, 19, 3 / 60), (20000, 7, 17, 13, 6.925 / 60)):
     lon = 30 + (rng.random(n) - 0.5) * (nx / 60 if fw < 0.1 else 0.3)
