@@ -52,6 +52,8 @@ def _load():
                                        ctypes.POINTER(OraMap), ctypes.c_double, ctypes.c_double,
                                        P, ctypes.c_int64, P, P, P, ctypes.c_int, ctypes.c_int]
         lib.ora_grid_cells.restype = ctypes.c_int
+        lib.ora_grid_cells_ex.argtypes = lib.ora_grid_cells.argtypes + [P, ctypes.c_int]
+        lib.ora_grid_cells_ex.restype = ctypes.c_int
         lib.ora_weight_tophat.argtypes = [ctypes.c_double] * 2
         lib.ora_weight_tophat.restype = ctypes.c_double
         lib.ora_neighbours.argtypes = [P, P, ctypes.c_int64, ctypes.POINTER(OraMap),
@@ -116,9 +118,11 @@ def cell_centre(m, i, j):
 
 
 def grid(lon, lat, vals, m, fwhm_deg, support=3.0, channels=None, cells=None, nthreads=0,
-         kernel="gaussian"):
+         kernel="gaussian", sample_weights=None, mask=False):
     """Eq. 1 for the given channels (rows of ``vals`` [C][N]) and cells; ``kernel`` is
-    "gaussian" (Eq. 1's kernel) or "tophat" (1 inside the support).
+    "gaussian" (Eq. 1's kernel) or "tophat" (SPEC.md:117-126: 1 inside the support);
+    ``sample_weights`` [N] multiply the kernel weight (reading R25); ``mask`` leaves
+    non-finite values out of both sums of their channel (reading R24).
 
     Returns (out [n_ch][n_cells] fp64 with NaN blanks, W [n_cells], nbr_count [n_cells]).
     ``cells`` = linear indices j*nx+i (None = all, in map order).
@@ -148,10 +152,13 @@ def grid(lon, lat, vals, m, fwhm_deg, support=3.0, channels=None, cells=None, nt
     out = np.empty((n_ch, n_cells), np.float64)
     W = np.empty(n_cells, np.float64)
     cnt = np.empty(n_cells, np.int64)
-    rc = _load().ora_grid_cells(_p(lon), _p(lat), n, _p(vals), ld, _p(ch), n_ch,
-                                ctypes.byref(mm), float(fwhm_deg), float(support),
-                                _p(cidx), n_cells, _p(out), _p(W), _p(cnt), int(nthreads),
-                                {"gaussian": 0, "tophat": 1}[kernel])
+    sw = None if sample_weights is None else np.ascontiguousarray(sample_weights, dtype=np.float64)
+    if sw is not None and sw.shape != (n,):
+        raise ValueError("sample_weights must have one entry per sample")
+    rc = _load().ora_grid_cells_ex(_p(lon), _p(lat), n, _p(vals), ld, _p(ch), n_ch,
+                                   ctypes.byref(mm), float(fwhm_deg), float(support),
+                                   _p(cidx), n_cells, _p(out), _p(W), _p(cnt), int(nthreads),
+                                   {"gaussian": 0, "tophat": 1}[kernel], _p(sw), int(bool(mask)))
     if rc != 0:
         raise ValueError(f"oracle rejected arguments (code {rc})")
     return out, W, cnt

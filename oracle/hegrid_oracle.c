@@ -130,15 +130,22 @@ static int valid_inputs(const ora_map* m, double fwhm, double support, int64_t n
  *   nbr_count  [n_cells] number of samples with d <= R; may be NULL
  *   nthreads   OpenMP threads (<= 0: runtime default)
  *   kind       0 = Gaussian (Eq. 1's kernel, readings R1-R3), 1 = tophat
+ *   sample_w   [n] per-sample weights omega_s >= 0 multiplying the kernel weight (NEXT-4,
+ *              DESIGN.md reading R25: w = omega_s w(d), W = sum_s omega_s w(d)); NULL = 1
+ *   mask       0: non-finite values enter the sums with IEEE semantics (reading R15);
+ *              1: a non-finite value is missing: it leaves both sums of its channel,
+ *              V_c = sum_{finite} w v / sum_{finite} w (reading R24); W stays sum_s w
  * Returns 0 on success, 1 on invalid arguments, 3 on allocation failure.
  */
-int ora_grid_cells(const double* lon, const double* lat, int64_t n,
-                   const float* vals, int64_t ld, const int64_t* ch_idx, int64_t n_ch,
-                   const ora_map* m, double fwhm_deg, double support,
-                   const int64_t* cell_idx, int64_t n_cells,
-                   double* out, double* wsum, int64_t* nbr_count, int nthreads, int kind) {
+int ora_grid_cells_ex(const double* lon, const double* lat, int64_t n,
+                      const float* vals, int64_t ld, const int64_t* ch_idx, int64_t n_ch,
+                      const ora_map* m, double fwhm_deg, double support,
+                      const int64_t* cell_idx, int64_t n_cells,
+                      double* out, double* wsum, int64_t* nbr_count, int nthreads, int kind,
+                      const double* sample_w, int mask) {
     if (!valid_inputs(m, fwhm_deg, support, n)) return 1;
     if (kind != 0 && kind != 1) return 1;
+    if (mask != 0 && mask != 1) return 1;
     if (n_ch < 0 || (n_ch > 0 && !vals) || (n > 0 && (!lon || !lat))) return 1;
     int64_t ncell_all = (int64_t)m->nx * (int64_t)m->ny;
     if (!cell_idx) n_cells = ncell_all;
@@ -166,6 +173,8 @@ int ora_grid_cells(const double* lon, const double* lat, int64_t n,
             double lon_c, lat_c;
             ora_cell_centre(m, i, j, &lon_c, &lat_c);
             int64_t k = cell_neighbours(lon, lat, n, lon_c, lat_c, sigma, R, kind, idx, w);
+            if (sample_w)
+                for (int64_t t = 0; t < k; ++t) w[t] *= sample_w[idx[t]];
             double W = 0.0;
             for (int64_t t = 0; t < k; ++t) W += w[t];
             if (wsum) wsum[q] = W;
@@ -174,9 +183,15 @@ int ora_grid_cells(const double* lon, const double* lat, int64_t n,
                 for (int64_t c = 0; c < n_ch; ++c) {
                     int64_t ch = ch_idx ? ch_idx[c] : c;
                     const float* row = vals + ch * ld;
-                    double S = 0.0;
-                    for (int64_t t = 0; t < k; ++t) S += w[t] * (double)row[idx[t]];
-                    out[c * n_cells + q] = (W > 0.0) ? S / W : NAN;
+                    double S = 0.0, Wc = 0.0;
+                    for (int64_t t = 0; t < k; ++t) {
+                        double v = (double)row[idx[t]];
+                        if (mask && !isfinite(v)) continue;
+                        S += w[t] * v;
+                        Wc += w[t];
+                    }
+                    double Wv = mask ? Wc : W;
+                    out[c * n_cells + q] = (Wv > 0.0) ? S / Wv : NAN;
                 }
             }
         }
@@ -184,6 +199,15 @@ int ora_grid_cells(const double* lon, const double* lat, int64_t n,
         free(w);
     }
     return failed ? 3 : 0;
+}
+
+int ora_grid_cells(const double* lon, const double* lat, int64_t n,
+                   const float* vals, int64_t ld, const int64_t* ch_idx, int64_t n_ch,
+                   const ora_map* m, double fwhm_deg, double support,
+                   const int64_t* cell_idx, int64_t n_cells,
+                   double* out, double* wsum, int64_t* nbr_count, int nthreads, int kind) {
+    return ora_grid_cells_ex(lon, lat, n, vals, ld, ch_idx, n_ch, m, fwhm_deg, support, cell_idx,
+                             n_cells, out, wsum, nbr_count, nthreads, kind, NULL, 0);
 }
 
 /*

@@ -362,3 +362,50 @@ def test_tophat_kernel_is_plain_neighbour_mean():
     og, Wg, cg = oracle.grid(lon, lat, v, m, fwhm)
     np.testing.assert_array_equal(cg, cnt)
     assert np.all((Wg > 0) == (W > 0))
+
+
+# ------------------------------------------------------------------ NEXT-4 variants (readings R24, R25)
+def test_integer_sample_weights_equal_duplicated_samples():
+    """Per-sample weights multiply the kernel weight (R25): an integer weight k gives exactly
+    what k copies of the sample give (0 removes it) -- a pin by construction, not by formula."""
+    rng = np.random.default_rng(25)
+    n = 300
+    lon = 30 + (rng.random(n) - 0.5) * 0.2
+    lat = 41 + (rng.random(n) - 0.5) * 0.2
+    vals = (10 + rng.standard_normal((2, n))).astype(np.float32)
+    wgt = rng.integers(0, 4, n)
+    m = {"nx": 9, "ny": 8, "crval_lon": 30.0, "crval_lat": 41.0, "crpix_x": 5.0, "crpix_y": 4.5,
+         "cdelt_lon": 0.02, "cdelt_lat": 0.02}
+    o, W, _ = oracle.grid(lon, lat, vals, m, 0.05, sample_weights=wgt.astype(np.float64))
+    rep = np.repeat(np.arange(n), wgt)
+    o2, W2, _ = oracle.grid(lon[rep], lat[rep], vals[:, rep], m, 0.05)
+    np.testing.assert_allclose(W, W2, rtol=1e-13, atol=0)
+    np.testing.assert_array_equal(np.isnan(o), np.isnan(o2))
+    ok = ~np.isnan(o)
+    np.testing.assert_allclose(o[ok], o2[ok], rtol=1e-12)
+
+
+def test_mask_equals_removing_the_masked_sample_from_its_channel():
+    """Masking (R24): a non-finite value leaves both sums of its channel -- channel c's map
+    equals the map gridded without the masked samples of c; the weight map keeps them."""
+    rng = np.random.default_rng(24)
+    n = 400
+    lon = 30 + (rng.random(n) - 0.5) * 0.2
+    lat = 41 + (rng.random(n) - 0.5) * 0.2
+    vals = (10 + rng.standard_normal((3, n))).astype(np.float32)
+    vals[0, rng.choice(n, 40, replace=False)] = np.nan
+    vals[2, rng.choice(n, 15, replace=False)] = np.inf
+    m = {"nx": 9, "ny": 8, "crval_lon": 30.0, "crval_lat": 41.0, "crpix_x": 5.0, "crpix_y": 4.5,
+         "cdelt_lon": 0.02, "cdelt_lat": 0.02}
+    o, W, _ = oracle.grid(lon, lat, vals, m, 0.05, mask=True)
+    _, Wp, _ = oracle.grid(lon, lat, vals, m, 0.05)
+    np.testing.assert_array_equal(W, Wp)
+    for c in range(3):
+        keep = np.isfinite(vals[c])
+        oc, _, _ = oracle.grid(lon[keep], lat[keep], vals[c:c + 1, keep], m, 0.05)
+        np.testing.assert_array_equal(np.isnan(o[c]), np.isnan(oc[0]))
+        ok = ~np.isnan(oc[0])
+        np.testing.assert_allclose(o[c][ok], oc[0][ok], rtol=1e-13)
+    # propagate (R15): a NaN makes every cell within R NaN
+    op, _, _ = oracle.grid(lon, lat, vals, m, 0.05)
+    assert np.isnan(op[0]).sum() > np.isnan(o[0]).sum()
