@@ -110,8 +110,20 @@ typedef struct hegrid_opts {
                                (weights computed in every launch).  A plan whose image did not
                                fit retries on later calls. */
     int32_t index;          /* hegrid_index: the plan's spatial index */
-    int32_t reserved;       /* must be 0 */
+    int32_t nonfinite;      /* hegrid_nonfinite: how non-finite sample values enter Eq. 1 */
 } hegrid_opts;
+
+/* Non-finite sample values (NaN, +-Inf; flagged spectra are common in single-dish data).
+ * PROPAGATE (default): IEEE arithmetic in Eq. 1 -- every cell within R of the sample gets
+ *       NaN (or +-Inf) in that channel, as the fp64 definition does.
+ * MASK: the value is missing: it is left out of both sums of its channel,
+ *       V_c = sum_{n: v_cn finite} w v_cn / sum_{n: v_cn finite} w, NaN where no finite value
+ *       remains; weight_map stays the channel-independent W = sum_n w (NEXT-4, SURVEY.md
+ *       8(f)).  The cells affected by a masked value are recomputed after the launch. */
+typedef enum hegrid_nonfinite {
+    HEGRID_NONFINITE_PROPAGATE = 0,
+    HEGRID_NONFINITE_MASK = 1
+} hegrid_nonfinite;
 
 /* Spatial index of a plan (the LUT of PAPER.md:177-192, sec. 3.1.1, Fig. 4/5).
  * BINS: map-aligned lon/lat bins, one per cell (rows of bins are contiguous sample ranges);
@@ -184,6 +196,16 @@ void hegrid_plan_destroy(hegrid_plan_t plan);
 
 /* Statistics; computes the pair counts on first call (one extra device pass). */
 hegrid_status hegrid_plan_info(hegrid_plan_t plan, hegrid_plan_stats* out);
+
+/* Per-sample weights (NEXT-4; reading R25): omega[n] >= 0 multiplies sample n's kernel
+ * weight, w = omega_n w(d), so V = sum omega w v / sum omega w and W = sum omega w (e.g.
+ * inverse noise variances of the spectra).  omega: host array of the
+ * plan's n samples in original order, borrowed for the call; NULL restores omega = 1.  The
+ * neighbour sets (hegrid_neighbours) stay geometric.  Drops the engine's per-plan tables
+ * (they are rebuilt by the next grid call); the caller serialises it with the plan's other
+ * calls.  Errors: EINVAL (n differs from the plan's), EDOMAIN (a weight non-finite or < 0),
+ * ECUDA, ENOMEM. */
+hegrid_status hegrid_plan_set_sample_weights(hegrid_plan_t plan, const float* omega, int64_t n);
 
 /* Plan order: perm[p] = original index of the sample at plan position p, p < n_used
  * (host array of n_used entries; *n_used may be NULL). */

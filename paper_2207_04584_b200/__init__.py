@@ -16,7 +16,8 @@ from ._binding import (HEGRID_ENGINE_TC, HEGRID_LAYOUT_PLAN_NC, HEGRID_LAYOUT_US
                        hegrid_pipeline_trace, hegrid_plan_info, hegrid_plan_permutation,
                        hegrid_profile_enable,
                        hegrid_profile_read, hegrid_sort_u32, hegrid_status_string, make_map,
-                       make_opts, hegrid_healpix_ang2pix, INDEXES)
+                       make_opts, hegrid_healpix_ang2pix, hegrid_plan_set_sample_weights, INDEXES,
+                       NONFINITE)
 from .shard import channel_shard  # noqa: F401
 
 __all__ = ["Plan", "abi", "channel_shard", "HegridError"]
@@ -43,12 +44,12 @@ class Plan:
 
     def __init__(self, lon, lat, map, fwhm_deg, support_sigma=3.0, device=0, n_streams=0,
                  channel_block=0, stream=None, engine="auto", kernel="gaussian",
-                 weight_image_max_bytes=0, index="auto"):
+                 weight_image_max_bytes=0, index="auto", nonfinite="propagate"):
         self.map = dict(map) if isinstance(map, dict) else map
         self.nx, self.ny = int(self.map["nx"]), int(self.map["ny"])
         self.device = device
         opts = make_opts(device, n_streams, channel_block, self.ENGINES[engine],
-                         weight_image_max_bytes, INDEXES[index])
+                         weight_image_max_bytes, INDEXES[index], NONFINITE[nonfinite])
         if hasattr(lon, "is_cuda") and lon.is_cuda:
             import torch
             lon = lon.to(torch.float64).contiguous()
@@ -93,6 +94,13 @@ class Plan:
     # -------------------------------------------------------------- queries
     def info(self) -> dict:
         return hegrid_plan_info(self._h)
+
+    def set_sample_weights(self, omega):
+        """Per-sample weights omega[n] >= 0 (original order) multiplying the kernel weight
+        (hegrid_plan_set_sample_weights); None restores 1."""
+        if omega is not None and hasattr(omega, "detach"):
+            omega = omega.detach().cpu().numpy()
+        hegrid_plan_set_sample_weights(self._h, omega)
 
     def permutation(self) -> np.ndarray:
         return hegrid_plan_permutation(self._h)

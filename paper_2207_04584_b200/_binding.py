@@ -50,7 +50,7 @@ class hegrid_opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("n_streams", ctypes.c_int32),
                 ("channel_block", ctypes.c_int32), ("engine", ctypes.c_int32),
                 ("weight_image_max_bytes", ctypes.c_int64), ("index", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("nonfinite", ctypes.c_int32)]
 
 
 class hegrid_plan_stats(ctypes.Structure):
@@ -91,6 +91,7 @@ SIGNATURES = {
     "hegrid_neighbours": (I32, [PLAN, I64, I64, P, P]),
     "hegrid_sort_u32": (I32, [P, I64, P, I32]),
     "hegrid_healpix_ang2pix": (I32, [I32, P, P, I64, P, I32]),
+    "hegrid_plan_set_sample_weights": (I32, [PLAN, P, I64]),
     "hegrid_profile_enable": (I32, [PLAN, I32]),
     "hegrid_profile_read": (I32, [PLAN, P, P]),
     "hegrid_pipeline_trace": (I32, [PLAN, P, I64, P]),
@@ -154,9 +155,15 @@ HEGRID_INDEX_AUTO, HEGRID_INDEX_BINS, HEGRID_INDEX_HEALPIX = 0, 1, 2
 INDEXES = {"auto": HEGRID_INDEX_AUTO, "bins": HEGRID_INDEX_BINS, "healpix": HEGRID_INDEX_HEALPIX}
 
 
+HEGRID_NONFINITE_PROPAGATE, HEGRID_NONFINITE_MASK = 0, 1
+NONFINITE = {"propagate": HEGRID_NONFINITE_PROPAGATE, "mask": HEGRID_NONFINITE_MASK}
+
+
 def make_opts(device=0, n_streams=0, channel_block=0, engine=0,
-              weight_image_max_bytes=0, index=HEGRID_INDEX_AUTO) -> hegrid_opts:
-    return hegrid_opts(device, n_streams, channel_block, engine, weight_image_max_bytes, index, 0)
+              weight_image_max_bytes=0, index=HEGRID_INDEX_AUTO,
+              nonfinite=HEGRID_NONFINITE_PROPAGATE) -> hegrid_opts:
+    return hegrid_opts(device, n_streams, channel_block, engine, weight_image_max_bytes, index,
+                       nonfinite)
 
 
 # ----------------------------------------------------------------- C-ABI names
@@ -238,6 +245,15 @@ def hegrid_sort_u32(keys: np.ndarray, device: int = 0) -> np.ndarray:
     perm = np.empty(k.shape[0], np.int32)
     _check(load().hegrid_sort_u32(_ptr(k), k.shape[0], _ptr(perm), device), "hegrid_sort_u32")
     return perm
+
+
+def hegrid_plan_set_sample_weights(plan: int, omega) -> None:
+    """Per-sample weights (original sample order) multiplying the kernel weight; None = 1."""
+    if omega is None:
+        _check(load().hegrid_plan_set_sample_weights(plan, None, 0), "hegrid_plan_set_sample_weights")
+        return
+    w = np.ascontiguousarray(omega, np.float32)
+    _check(load().hegrid_plan_set_sample_weights(plan, _ptr(w), w.shape[0]), "hegrid_plan_set_sample_weights")
 
 
 def hegrid_healpix_ang2pix(nside: int, theta: np.ndarray, phi: np.ndarray, device: int = 0) -> np.ndarray:

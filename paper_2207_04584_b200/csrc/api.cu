@@ -201,7 +201,8 @@ hegrid_status hegrid_plan_create(const double* lon_deg, const double* lat_deg, i
     if (n > 0 && (!lon_deg || !lat_deg)) return HEGRID_EINVAL;
     HG_TRY_S(validate_geometry(map, kernel));
     hegrid_opts o = default_opts(opts);
-    if (o.index < 0 || o.reserved != 0) return HEGRID_EINVAL;
+    if (o.index < 0 || (o.nonfinite != HEGRID_NONFINITE_PROPAGATE && o.nonfinite != HEGRID_NONFINITE_MASK))
+        return HEGRID_EINVAL;
     DeviceGuard dg(o.device);
     HG_TRY(dg.err);
     // coordinates H2D into stream-ordered buffers of the device pool (no cudaMalloc / cudaFree
@@ -243,7 +244,8 @@ hegrid_status hegrid_plan_create_device(const double* d_lon, const double* d_lat
     if (n > 0 && (!d_lon || !d_lat)) return HEGRID_EINVAL;
     HG_TRY_S(validate_geometry(map, kernel));
     hegrid_opts o = default_opts(opts);
-    if (o.index < 0 || o.reserved != 0) return HEGRID_EINVAL;
+    if (o.index < 0 || (o.nonfinite != HEGRID_NONFINITE_PROPAGATE && o.nonfinite != HEGRID_NONFINITE_MASK))
+        return HEGRID_EINVAL;
     DeviceGuard dg(o.device);
     HG_TRY(dg.err);
     return create_common(d_lon, d_lat, n, map, kernel, o, (cudaStream_t)stream, out);
@@ -258,7 +260,7 @@ void hegrid_plan_destroy(hegrid_plan_t p) {
     for (void* q : {(void*)p->d_keys, (void*)p->d_perm, (void*)p->d_iperm, (void*)p->d_geo,
                     (void*)p->d_ll, (void*)p->d_bin_start, (void*)p->d_mrow, (void*)p->d_cos_row,
                     (void*)p->d_tc_sched, (void*)p->d_tc_tile_off, (void*)p->d_tc_wsum,
-                    (void*)p->d_tc_wimg, (void*)p->d_tc_wslot})
+                    (void*)p->d_tc_wimg, (void*)p->d_tc_wslot, (void*)p->d_omega})
         if (q) cudaFreeAsync(q, 0);
     for (auto e : p->prof_events) cudaEventDestroy(e);
     for (auto& x : p->slots) {
@@ -273,6 +275,54 @@ void hegrid_plan_destroy(hegrid_plan_t p) {
     cudaStreamSynchronize(0);
     delete p;
     phase_mark("plan_destroy: done");
+}
+
+__global__ void k_gather_omega(const float* __restrict__ w, const int32_t* __restrict__ perm,
+                               int64_t n_used, float* __restrict__ dst) {
+    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q < n_used) dst[q] = w[perm[q]];
+}
+
+hegrid_status hegrid_plan_set_sample_weights(hegrid_plan_t p, const float* omega, int64_t n) {
+    if (!p || (omega && n != p->n)) return HEGRID_EINVAL;
+    if (omega)
+        for (int64_t k = 0; k < n; ++k)
+            if (!(omega[k] >= 0.0f) || !isfinite(omega[k])) return HEGRID_EDOMAIN;
+    DeviceGuard dg(p->device);
+    HG_TRY(dg.err);
+    HG_TRY(cudaDeviceSynchronize());
+    // the engine tables that hold weights (W per cell, the weight image) are rebuilt lazily;
+    // the tensor-core schedule is geometric but is rebuilt with them
+    for (void* q : {(void*)p->d_tc_sched, (void*)p->d_tc_tile_off, (void*)p->d_tc_wsum,
+                    (void*)p->d_tc_wimg, (void*)p->d_tc_wslot})
+        if (q) cudaFreeAsync(q, 0);
+    p->d_tc_sched = nullptr;
+    p->d_tc_tile_off = nullptr;
+    p->d_tc_wsum = nullptr;
+    p->d_tc_wimg = nullptr;
+    p->d_tc_wslot = nullptr;
+    p->tc_nchunks = -1;
+    p->tc_pw = -1;
+    p->tc_wimg_bytes = 0;
+    if (p->d_omega) cudaFreeAsync(p->d_omega, 0);
+    p->d_omega = nullptr;
+    if (!omega || p->n_used == 0) return cuda_status(cudaStreamSynchronize(0));
+    float* d_w = nullptr;
+    HG_TRY(plan_alloc(p, &d_w, n * sizeof(float), 0));
+    cudaError_t e = plan_alloc(p, &p->d_omega, p->n_used * sizeof(float), 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_w, omega, n * sizeof(float), cudaMemcpyHostToDevice, 0);
+    if (e == cudaSuccess) {
+        k_gather_omega<<<(unsigned)((p->n_used + 255) / 256), 256, 0, 0>>>(d_w, p->d_perm, p->n_used, p->d_omega);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(d_w, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+    if (e != cudaSuccess && p->d_omega) {
+        cudaFreeAsync(p->d_omega, 0);
+        p->d_omega = nullptr;
+    }
+    return cuda_status(e);
 }
 
 hegrid_status hegrid_plan_info(hegrid_plan_t p, hegrid_plan_stats* out) {

@@ -54,6 +54,7 @@ struct PlanDev {
     const uint32_t* bin_start;  // [nbins + 1]
     const int* mrow;            // [nrow] lon reach (bins) of a cell for samples in that bin row
     const float* cos_row;       // [ny] cos(lat) of cell rows (fp32)
+    const float* omega;         // [n_used] per-sample weights in plan order (nullptr = all 1)
 };
 
 }  // namespace hg
@@ -76,6 +77,7 @@ struct hegrid_plan_s {
     uint32_t* d_bin_start = nullptr;
     int* d_mrow = nullptr;
     float* d_cos_row = nullptr;
+    float* d_omega = nullptr;       // per-sample weights, plan order (hegrid_plan_set_sample_weights)
     double t_plan_ms = 0;
     int64_t max_cand = 0;           // max candidate-range length over cells
     bool stats_valid = false;
@@ -120,7 +122,7 @@ struct hegrid_plan_s {
     std::vector<double> trace;
 
     hg::PlanDev dev() const {
-        return hg::PlanDev{d_geo, d_ll, d_bin_start, d_mrow, d_cos_row};
+        return hg::PlanDev{d_geo, d_ll, d_bin_start, d_mrow, d_cos_row, d_omega};
     }
 };
 

@@ -121,11 +121,12 @@ __global__ void __launch_bounds__(SIMT_THREADS, (QC == 4 && !SPLIT) ? 2 : 1) k_a
                 float w[8];
                 if (s < s1) {
                     const float4 geo = pd.geo[s];
+                    const float om = pd.omega ? __ldg(&pd.omega[s]) : 1.0f;   // reading R25
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         const int c = k % BW, r = k / BW;
                         w[k] = (cok[c] && rok[r])
-                                   ? pair_weight(g, pd, bi0 + c, bj0 + r, cosc[r], br, geo, (int)s)
+                                   ? __fmul_rn(pair_weight(g, pd, bi0 + c, bj0 + r, cosc[r], br, geo, (int)s), om)
                                    : 0.0f;
                     }
                 } else {

@@ -196,6 +196,14 @@ __device__ __forceinline__ void entry_weights(const Geom& g, const PlanDev& pd, 
             if (by == k) cos_c = cosr[k];
         float w[4][2];                 // [sample][cell col]
         patch_weights<2>(g, pd, row, cj, ci0, 2 * ch2, cos_c, g4, pstart + 4 * kq, w);
+        if (pd.omega) {                // per-sample weights (reading R25): w = omega_n w(d)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float om = w[u][0] > 0.0f || w[u][1] > 0.0f ? __ldg(&pd.omega[pstart + 4 * kq + u]) : 0.0f;
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) w[u][cc] = __fmul_rn(w[u][cc], om);
+            }
+        }
         if (cj >= g.ny) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
@@ -364,7 +372,8 @@ __global__ void k_tc_wsum(const __grid_constant__ Geom g, PlanDev pd, float* __r
             float w[4][4];
             patch_weights<4>(g, pd, br, j, ci0, 0, cos_c, sv, s, w);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) part += w[u][cc];
+            for (int u = 0; u < 4; ++u)
+                part += pd.omega && w[u][cc] > 0.0f ? __fmul_rn(w[u][cc], __ldg(&pd.omega[s + u])) : w[u][cc];
         }
         const float y = part - Wc;
         const float t = W + y;

@@ -36,6 +36,7 @@ struct HpxGeom {
     double crval_lon, crval_lat, crpix_x, crpix_y, cdelt_lon, cdelt_lat;
     double R, sigma;      // rad
     int tophat;
+    int mask;             // HEGRID_NONFINITE_MASK: non-finite values leave both sums of their channel
 };
 
 __device__ __forceinline__ void hpx_cell(const HpxGeom& h, int64_t cell, double* lon, double* lat) {
@@ -138,7 +139,8 @@ __device__ __forceinline__ double hpx_weight(const HpxGeom& h, double clon, doub
 
 __global__ void __launch_bounds__(HPX_THREADS)
 k_hpx_grid(const HpxGeom h, const uint32_t* __restrict__ keys, uint32_t n,
-           const double2* __restrict__ ll, const float* __restrict__ v, int64_t ldv, int C,
+           const double2* __restrict__ ll, const float* __restrict__ omega,
+           const float* __restrict__ v, int64_t ldv, int C,
            float* __restrict__ out, float* __restrict__ wout) {
     __shared__ uint32_t rb[HPX_MAX_RANGES], re[HPX_MAX_RANGES];
     __shared__ double ws[HPX_THREADS];
@@ -154,7 +156,7 @@ k_hpx_grid(const HpxGeom h, const uint32_t* __restrict__ keys, uint32_t n,
     hpx_ring_span(h, theta_c, &r0, &r1);
     if (threadIdx.x == 0) s_ring = r0;
     __syncthreads();
-    double S = 0.0, W = 0.0;
+    double S = 0.0, W = 0.0, Wc = 0.0;
     for (;;) {
         if (threadIdx.x < 32) {
             int ring = s_ring;
@@ -171,7 +173,10 @@ k_hpx_grid(const HpxGeom h, const uint32_t* __restrict__ keys, uint32_t n,
             for (uint32_t b0 = rb[q]; b0 < re[q]; b0 += HPX_THREADS) {
                 const uint32_t s = b0 + threadIdx.x;
                 double w = -1.0;
-                if (s < re[q]) w = hpx_weight(h, clon, clat, cosc, __ldg(&ll[s]));
+                if (s < re[q]) {
+                    w = hpx_weight(h, clon, clat, cosc, __ldg(&ll[s]));
+                    if (omega && w >= 0.0) w *= (double)__ldg(&omega[s]);   // reading R25
+                }
                 ws[threadIdx.x] = w;
                 ss[threadIdx.x] = s;
                 __syncthreads();
@@ -180,7 +185,13 @@ k_hpx_grid(const HpxGeom h, const uint32_t* __restrict__ keys, uint32_t n,
                     const double wk = ws[k];
                     if (wk >= 0.0) {
                         W += wk;
-                        if (ch < C) S += wk * (double)__ldg(&v[(int64_t)ss[k] * ldv + ch]);
+                        if (ch < C) {
+                            const float vk = __ldg(&v[(int64_t)ss[k] * ldv + ch]);
+                            if (!h.mask || isfinite(vk)) {
+                                S += wk * (double)vk;
+                                Wc += wk;
+                            }
+                        }
                     }
                 }
                 __syncthreads();
@@ -190,7 +201,8 @@ k_hpx_grid(const HpxGeom h, const uint32_t* __restrict__ keys, uint32_t n,
         __syncthreads();
     }
     const int64_t cells = (int64_t)h.nx * h.ny;
-    if (ch < C) out[(int64_t)ch * cells + cell] = W > 0.0 ? (float)(S / W) : __int_as_float(0x7fc00000);
+    const double Wv = h.mask ? Wc : W;
+    if (ch < C) out[(int64_t)ch * cells + cell] = Wv > 0.0 ? (float)(S / Wv) : __int_as_float(0x7fc00000);
     if (wout && blockIdx.y == 0 && threadIdx.x == 0) wout[cell] = (float)W;
 }
 
@@ -258,6 +270,7 @@ static HpxGeom hpx_geom(const hegrid_plan_s* p) {
     h.sigma = p->kern.fwhm_deg / (2.0 * sqrt(2.0 * log(2.0))) * kDeg2Rad;
     h.R = p->kern.support_sigma * h.sigma;
     h.tophat = p->kern.kind == HEGRID_KERNEL_TOPHAT;
+    h.mask = p->opts.nonfinite == HEGRID_NONFINITE_MASK;
     return h;
 }
 
@@ -319,7 +332,7 @@ hegrid_status launch_accumulate_hpx(const hegrid_plan_s* p, const float* d_v, in
     const dim3 grid((unsigned)cells, (unsigned)((n_channels + HPX_THREADS - 1) / HPX_THREADS));
     if (grid.y > 65535) return HEGRID_EINVAL;
     k_hpx_grid<<<grid, HPX_THREADS, 0, st>>>(hpx_geom(p), p->d_keys, (uint32_t)p->n_used, p->d_ll,
-                                             d_v, ldv, (int)n_channels, d_out, d_weight);
+                                             p->d_omega, d_v, ldv, (int)n_channels, d_out, d_weight);
     count_launch();
     return cuda_status(cudaGetLastError());
 }

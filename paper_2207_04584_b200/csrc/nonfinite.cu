@@ -75,6 +75,82 @@ __global__ void k_nonfinite_fix(const __grid_constant__ Geom g, PlanDev pd,
     }
 }
 
+// HEGRID_NONFINITE_MASK: the cells within R of a recorded non-finite value (p, c) get channel
+// c's Eq. 1 recomputed over the finite values only (one warp per cell, fp64 sums over the
+// cell's candidate ranges with the SIMT engine's pair_weight):
+//   V_c = sum_{n: v_cn finite} w v_cn / sum_{n: v_cn finite} w,   NaN if no finite value.
+// Records that hit the same (cell, channel) recompute the same value (idempotent writes).
+__device__ void nf_mask_cell(const Geom& g, const PlanDev& pd, const float* __restrict__ V,
+                             int64_t ldv, int c, int i, int j, float* __restrict__ out, int lane) {
+    const float cos_c = pd.cos_row[j];
+    double S = 0.0, Wc = 0.0;
+    for (int br = j; br <= j + 2 * g.mlat; ++br) {
+        const int m = pd.mrow[br];
+        const int64_t rowb = (int64_t)br * g.ncol;
+        const uint32_t s0 = pd.bin_start[rowb + i + g.mlon - m];
+        const uint32_t s1 = pd.bin_start[rowb + i + g.mlon + m + 1];
+        for (uint32_t s = s0 + lane; s < s1; s += 32) {
+            float w = pair_weight(g, pd, i, j, cos_c, br, pd.geo[s], (int)s);
+            if (pd.omega && w > 0.0f) w = __fmul_rn(w, pd.omega[s]);
+            if (w > 0.0f) {
+                const float v = V[(int64_t)s * ldv + c];
+                if (!nf_bad(v)) {
+                    S += (double)w * v;
+                    Wc += w;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        S += __shfl_xor_sync(0xffffffffu, S, o);
+        Wc += __shfl_xor_sync(0xffffffffu, Wc, o);
+    }
+    if (lane == 0) {
+        const int64_t cells = (int64_t)g.nx * g.ny;
+        out[(int64_t)c * cells + (int64_t)j * g.nx + i] = Wc > 0.0 ? (float)(S / Wc) : __int_as_float(0x7fc00000);
+    }
+}
+
+// the cells within R of the sample at plan position p (the engines' predicate), one warp each
+__device__ void nf_mask_apply(const Geom& g, const PlanDev& pd, const uint32_t* __restrict__ keys,
+                              const float* __restrict__ V, int64_t ldv, uint32_t p, int c,
+                              float* __restrict__ out, int warp, int nwarps, int lane) {
+    const uint32_t key = keys[p];
+    const int br = (int)(key / (uint32_t)g.ncol), bc = (int)(key % (uint32_t)g.ncol);
+    const int m = pd.mrow[br];
+    const int j0 = max(0, br - g.mlat - g.rl), j1 = min(g.ny - 1, br - g.mlat + g.rl);
+    const int i0 = max(0, bc - g.mlon - m), i1 = min(g.nx - 1, bc - g.mlon + m);
+    const int ni = i1 - i0 + 1;
+    if (ni <= 0 || j1 < j0) return;
+    for (int q = warp; q < (j1 - j0 + 1) * ni; q += nwarps) {
+        const int j = j0 + q / ni, i = i0 + q % ni;
+        const float w = pair_weight(g, pd, i, j, pd.cos_row[j], br, pd.geo[p], (int)p);
+        if (w > 0.0f) nf_mask_cell(g, pd, V, ldv, c, i, j, out, lane);
+    }
+}
+
+__global__ void __launch_bounds__(128)
+k_nonfinite_mask(const __grid_constant__ Geom g, PlanDev pd, const uint32_t* __restrict__ keys,
+                 const float* __restrict__ V, int64_t ldv, int C, int64_t n_used, NfBuf nf,
+                 float* __restrict__ out) {
+    const uint32_t count = nf.hdr[0], overflow = nf.hdr[1];
+    if (count == 0) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (!overflow) {
+        for (int64_t r = blockIdx.x; r < (int64_t)min(count, kNfCap); r += gridDim.x) {
+            const unsigned long long e = nf.rec[r];
+            nf_mask_apply(g, pd, keys, V, ldv, (uint32_t)e, (int)(e >> 32), out, warp, 4, lane);
+        }
+    } else {   // too many records: scan every value
+        for (int64_t e = blockIdx.x; e < n_used * C; e += gridDim.x) {
+            const int64_t p = e / C;
+            const int c = (int)(e % C);
+            if (nf_bad(V[p * ldv + c])) nf_mask_apply(g, pd, keys, V, ldv, (uint32_t)p, c, out, warp, 4, lane);
+        }
+    }
+}
+
 hegrid_status nonfinite_alloc(const hegrid_plan_s* p, NfBuf* nf, cudaStream_t st) {
     void* b = nullptr;
     HG_TRY(plan_alloc(p, &b, 16 + (size_t)kNfCap * 8, st));
@@ -88,8 +164,12 @@ hegrid_status nonfinite_alloc(const hegrid_plan_s* p, NfBuf* nf, cudaStream_t st
 // was recorded), then release the buffer.
 hegrid_status nonfinite_fix(const hegrid_plan_s* p, const float* d_v, int64_t ldv, int C, NfBuf nf,
                             float* d_out, cudaStream_t st) {
-    k_nonfinite_fix<<<4 * 148, 128, 0, st>>>(p->g, p->dev(), p->d_keys, d_v, ldv, C, p->n_used,
-                                             nf, d_out);
+    if (p->opts.nonfinite == HEGRID_NONFINITE_MASK)
+        k_nonfinite_mask<<<4 * 148, 128, 0, st>>>(p->g, p->dev(), p->d_keys, d_v, ldv, C, p->n_used,
+                                                  nf, d_out);
+    else
+        k_nonfinite_fix<<<4 * 148, 128, 0, st>>>(p->g, p->dev(), p->d_keys, d_v, ldv, C, p->n_used,
+                                                 nf, d_out);
     count_launch();
     HG_TRY(cudaGetLastError());
     HG_TRY(cudaFreeAsync(nf.hdr, st));

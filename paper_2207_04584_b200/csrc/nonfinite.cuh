@@ -9,7 +9,8 @@
 // (plan position, channel); after the launch, k_nonfinite_fix combines each recorded value
 // into the cells within its support, with IEEE semantics (NaN wins, +Inf with -Inf gives
 // NaN), order-independent.  Records that do not fit set the overflow flag, and the fix-up
-// then scans every value instead.
+// then scans every value instead.  With hegrid_opts.nonfinite = MASK the fix-up instead
+// recomputes the affected (cell, channel) values over the finite values only.
 #pragma once
 
 #include <float.h>
