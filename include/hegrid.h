@@ -69,7 +69,25 @@ typedef struct hegrid_map {
     double crval_lon, crval_lat;    /* deg */
     double crpix_x, crpix_y;        /* 1-based */
     double cdelt_lon, cdelt_lat;    /* deg per cell */
+    int32_t projection;             /* hegrid_projection */
+    int32_t reserved;               /* must be 0 */
 } hegrid_map;
+
+/* Cell centres of the map (reading R26).  Intermediate world coordinates of cell (i, j):
+ * x = (i + 1 - crpix_x) cdelt_lon, y = (j + 1 - crpix_y) cdelt_lat (deg).
+ * CAR: the linear lon/lat grid of the paper's "regular, uniform grid" (reading
+ *      R6): lon = crval_lon + x, lat = crval_lat + y.
+ * TAN / SIN: the zenithal gnomonic / orthographic projections of the FITS WCS standard
+ *      (Calabretta & Greisen 2002) with the reference point (crval_lon, crval_lat) at the
+ *      native pole and LONPOLE = 180 deg: the cell lies at great-circle distance atan(r)
+ *      (TAN) or asin(r) (SIN) from the reference point, r = sqrt(x^2 + y^2) in radians,
+ *      in the direction of position angle atan2(x, y) (NEXT-4).  Projected maps are served
+ *      by the HEALPix index (the lon/lat bins need CAR). */
+typedef enum hegrid_projection {
+    HEGRID_PROJ_CAR = 0,
+    HEGRID_PROJ_TAN = 1,
+    HEGRID_PROJ_SIN = 2
+} hegrid_projection;
 
 /* Convolution kernel w(d) of the great-circle distance d (readings R1-R3; SPEC.md:117-126
  * KernelSpec{kind, sigma, radius}): sigma = fwhm / (2 sqrt(2 ln 2)), support radius

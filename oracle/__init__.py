@@ -37,9 +37,11 @@ class OraMap(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32),
                 ("crval_lon", ctypes.c_double), ("crval_lat", ctypes.c_double),
                 ("crpix_x", ctypes.c_double), ("crpix_y", ctypes.c_double),
-                ("cdelt_lon", ctypes.c_double), ("cdelt_lat", ctypes.c_double)]
+                ("cdelt_lon", ctypes.c_double), ("cdelt_lat", ctypes.c_double),
+                ("projection", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
+PROJECTIONS = {"car": 0, "tan": 1, "sin": 2}
 _lib = None
 
 
@@ -79,11 +81,13 @@ def _load():
 
 
 def _map(m) -> OraMap:
-    """Accept any object/dict with the hegrid map fields."""
+    """Accept any object/dict with the hegrid map fields (optional "projection")."""
     g = (lambda k: m[k]) if isinstance(m, dict) else (lambda k: getattr(m, k))
+    proj = (m.get("projection", 0) if isinstance(m, dict) else getattr(m, "projection", 0))
+    proj = PROJECTIONS[proj] if isinstance(proj, str) else int(proj)
     return OraMap(int(g("nx")), int(g("ny")), float(g("crval_lon")), float(g("crval_lat")),
                   float(g("crpix_x")), float(g("crpix_y")), float(g("cdelt_lon")),
-                  float(g("cdelt_lat")))
+                  float(g("cdelt_lat")), proj, 0)
 
 
 def _p(a):

@@ -45,6 +45,8 @@ typedef struct {
     double crval_lon, crval_lat;
     double crpix_x, crpix_y;
     double cdelt_lon, cdelt_lat;
+    int32_t projection;     /* 0 linear lon/lat (R6), 1 TAN, 2 SIN (reading R26) */
+    int32_t reserved;
 } ora_map;
 
 static const double ORA_PI = 3.14159265358979323846;
@@ -62,10 +64,37 @@ double ora_wrap180(double x) {
     return y;
 }
 
-/* Cell centre of 0-based cell (i, j), reading R6. */
+/* Cell centre of 0-based cell (i, j).  Linear lon/lat grid (reading R6), or a zenithal
+ * projection (reading R26) written as in the FITS WCS definition (Calabretta & Greisen
+ * 2002, A&A 395, 1077): intermediate world coordinates x, y (deg); native longitude
+ * phi = arg(-y, x) (their eq. 14); native latitude theta = atan(180/pi / R) for TAN (eq. 54)
+ * or acos(pi/180 R) for SIN (eq. 59, R = sqrt(x^2 + y^2)); native -> celestial with the
+ * native pole at (crval_lon, crval_lat) and LONPOLE phi_p = 180 deg (eq. 2). */
 void ora_cell_centre(const ora_map* m, int64_t i, int64_t j, double* lon, double* lat) {
-    *lon = m->crval_lon + ((double)i + 1.0 - m->crpix_x) * m->cdelt_lon;
-    *lat = m->crval_lat + ((double)j + 1.0 - m->crpix_y) * m->cdelt_lat;
+    double x = ((double)i + 1.0 - m->crpix_x) * m->cdelt_lon;
+    double y = ((double)j + 1.0 - m->crpix_y) * m->cdelt_lat;
+    if (m->projection == 0) {
+        *lon = m->crval_lon + x;
+        *lat = m->crval_lat + y;
+        return;
+    }
+    double r = sqrt(x * x + y * y);
+    double phi = (r == 0.0) ? 0.0 : atan2(x, -y);
+    double theta;
+    if (m->projection == 1) {
+        theta = atan2(180.0 / ORA_PI, r);
+    } else {
+        double a = r * ORA_PI / 180.0;
+        theta = a <= 1.0 ? acos(a) : NAN;
+    }
+    double ap = deg2rad(m->crval_lon), dp = deg2rad(m->crval_lat), php = ORA_PI;
+    double sd = sin(theta) * sin(dp) + cos(theta) * cos(dp) * cos(phi - php);
+    if (sd > 1.0) sd = 1.0;
+    if (sd < -1.0) sd = -1.0;
+    double a = ap + atan2(-cos(theta) * sin(phi - php),
+                          sin(theta) * cos(dp) - cos(theta) * sin(dp) * cos(phi - php));
+    *lat = asin(sd) * 180.0 / ORA_PI;
+    *lon = a * 180.0 / ORA_PI;
 }
 
 /* Great-circle distance in radians, haversine form (reading R5). */

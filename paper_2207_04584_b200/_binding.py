@@ -34,7 +34,8 @@ class hegrid_map(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32),
                 ("crval_lon", ctypes.c_double), ("crval_lat", ctypes.c_double),
                 ("crpix_x", ctypes.c_double), ("crpix_y", ctypes.c_double),
-                ("cdelt_lon", ctypes.c_double), ("cdelt_lat", ctypes.c_double)]
+                ("cdelt_lon", ctypes.c_double), ("cdelt_lat", ctypes.c_double),
+                ("projection", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class hegrid_kernel(ctypes.Structure):
@@ -144,11 +145,16 @@ def _ptr(x):
     raise TypeError(type(x))
 
 
+PROJECTIONS = {"car": 0, "tan": 1, "sin": 2}
+
+
 def make_map(m) -> hegrid_map:
     g = (lambda k: m[k]) if isinstance(m, dict) else (lambda k: getattr(m, k))
+    proj = (m.get("projection", 0) if isinstance(m, dict) else getattr(m, "projection", 0))
+    proj = PROJECTIONS[proj] if isinstance(proj, str) else int(proj)
     return hegrid_map(int(g("nx")), int(g("ny")), float(g("crval_lon")), float(g("crval_lat")),
                       float(g("crpix_x")), float(g("crpix_y")), float(g("cdelt_lon")),
-                      float(g("cdelt_lat")))
+                      float(g("cdelt_lat")), proj, 0)
 
 
 HEGRID_INDEX_AUTO, HEGRID_INDEX_BINS, HEGRID_INDEX_HEALPIX = 0, 1, 2

@@ -65,6 +65,8 @@ static hegrid_status validate_geometry(const hegrid_map* m, const hegrid_kernel*
     for (double x : v)
         if (!isfinite(x)) return HEGRID_EINVAL;
     if (m->cdelt_lon == 0.0 || m->cdelt_lat == 0.0) return HEGRID_EINVAL;
+    if (m->projection < HEGRID_PROJ_CAR || m->projection > HEGRID_PROJ_SIN || m->reserved != 0)
+        return HEGRID_EINVAL;
     if (!(k->fwhm_deg > 0.0) || !(k->support_sigma > 0.0)) return HEGRID_EINVAL;
     if (k->kind != HEGRID_KERNEL_GAUSSIAN && k->kind != HEGRID_KERNEL_TOPHAT) return HEGRID_EINVAL;
     if (k->reserved != 0) return HEGRID_EINVAL;

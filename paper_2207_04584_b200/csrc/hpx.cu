@@ -37,12 +37,32 @@ struct HpxGeom {
     double R, sigma;      // rad
     int tophat;
     int mask;             // HEGRID_NONFINITE_MASK: non-finite values leave both sums of their channel
+    int projection;       // hegrid_projection
 };
 
+// Cell centre (hegrid.h, reading R26).  Projected maps: the cell lies at great-circle
+// distance rho = atan(r) (TAN) or asin(r) (SIN) from the reference point in the direction of
+// position angle pa = atan2(x, y) (east of north); the point at distance rho and bearing pa
+// from (lon0, lat0) follows from the spherical law of cosines.
 __device__ __forceinline__ void hpx_cell(const HpxGeom& h, int64_t cell, double* lon, double* lat) {
     const int i = (int)(cell % h.nx), j = (int)(cell / h.nx);
-    *lon = h.crval_lon + ((double)i + 1.0 - h.crpix_x) * h.cdelt_lon;
-    *lat = h.crval_lat + ((double)j + 1.0 - h.crpix_y) * h.cdelt_lat;
+    const double x = ((double)i + 1.0 - h.crpix_x) * h.cdelt_lon;
+    const double y = ((double)j + 1.0 - h.crpix_y) * h.cdelt_lat;
+    if (h.projection == HEGRID_PROJ_CAR) {
+        *lon = h.crval_lon + x;
+        *lat = h.crval_lat + y;
+        return;
+    }
+    const double r = sqrt(x * x + y * y) * kDeg2Rad;
+    const double rho = h.projection == HEGRID_PROJ_TAN ? atan(r) : (r <= 1.0 ? asin(r) : nan(""));
+    const double pa = atan2(x, y);
+    const double la0 = h.crval_lat * kDeg2Rad;
+    double sl = sin(la0) * cos(rho) + cos(la0) * sin(rho) * cos(pa);
+    sl = fmin(1.0, fmax(-1.0, sl));
+    const double la = asin(sl);
+    const double dlo = atan2(sin(pa) * sin(rho) * cos(la0), cos(rho) - sin(la0) * sl);
+    *lat = la / kDeg2Rad;
+    *lon = h.crval_lon + dlo / kDeg2Rad;
 }
 
 __global__ void k_hpx_keys(int64_t nside, const double* __restrict__ lon, const double* __restrict__ lat,
@@ -271,6 +291,7 @@ static HpxGeom hpx_geom(const hegrid_plan_s* p) {
     h.R = p->kern.support_sigma * h.sigma;
     h.tophat = p->kern.kind == HEGRID_KERNEL_TOPHAT;
     h.mask = p->opts.nonfinite == HEGRID_NONFINITE_MASK;
+    h.projection = p->map.projection;
     return h;
 }
 

@@ -241,6 +241,7 @@ static hegrid_status make_geom(hegrid_plan_s* p, std::vector<int>& mrow,
     double sigma_deg = p->kern.fwhm_deg / (2.0 * sqrt(2.0 * log(2.0)));
     double R_deg = p->kern.support_sigma * sigma_deg;
     if (R_deg > 1.0) return HEGRID_EUNSUPPORTED;
+    if (m.projection != HEGRID_PROJ_CAR) return HEGRID_EUNSUPPORTED;   // bins need a lon/lat grid
     g.sigma_rad = sigma_deg * kDeg2Rad;
     g.R_rad = R_deg * kDeg2Rad;
     const double eps = 1e-6;

@@ -96,3 +96,33 @@ def test_sample_weights_errors():
         with pytest.raises(HegridError) as e:
             p.set_sample_weights(bad)
         assert e.value.code == 2
+
+
+@pytest.mark.parametrize("proj", ["tan", "sin"])
+@pytest.mark.parametrize("wide", [False, True])
+def test_projected_maps(proj, wide):
+    """Zenithal TAN / SIN maps (reading R26): cell centres from the projection, gridded through
+    the HEALPix index (AUTO; the bin index refuses them), against the oracle's own projection
+    code -- values, W, blank pattern and the exact neighbour sets."""
+    rng = np.random.default_rng(26)
+    if wide:      # a 40 x 40 degree field at high latitude, R = 1.7 deg
+        n, cen, half, fw, cd, nx = 40000, (120.0, 62.0), 20.0, 1.33, 1.25, 33
+    else:         # a 1.3 x 1 degree field, R = 3.8 arcmin
+        n, cen, half, fw, cd, nx = 30000, (30.0, 41.0), 0.65, 0.05, 1 / 30, 41
+    lat = cen[1] + (rng.random(n) - 0.5) * 2 * half
+    lon = cen[0] + (rng.random(n) - 0.5) * 2 * half / np.cos(np.radians(cen[1]))
+    m = {"nx": nx, "ny": nx - 8, "crval_lon": cen[0], "crval_lat": cen[1], "crpix_x": (nx + 1) / 2,
+         "crpix_y": (nx - 7) / 2, "cdelt_lon": -cd, "cdelt_lat": cd, "projection": proj}
+    vals = (10 + rng.standard_normal((3, n))).astype(np.float32)
+    with pytest.raises(HegridError):
+        Plan(lon, lat, m, fw, index="bins")
+    with Plan(lon, lat, m, fw) as p:
+        assert p.info()["index"] == 2
+        out, W = p.grid(vals)
+        off, idx = p.neighbours()
+    o, Wo, _ = oracle.grid(lon, lat, vals, m, fw, 3.0)
+    st = compare(out, W, o, Wo)
+    assert st["covered"] > 0.5 * m["nx"] * m["ny"]
+    ooff, oidx = oracle.neighbours(lon, lat, m, fw, 3.0)
+    np.testing.assert_array_equal(off, ooff)
+    np.testing.assert_array_equal(idx, oidx)

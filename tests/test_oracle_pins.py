@@ -409,3 +409,32 @@ def test_mask_equals_removing_the_masked_sample_from_its_channel():
     # propagate (R15): a NaN makes every cell within R NaN
     op, _, _ = oracle.grid(lon, lat, vals, m, 0.05)
     assert np.isnan(op[0]).sum() > np.isnan(o[0]).sum()
+
+
+@pytest.mark.parametrize("proj", ["tan", "sin"])
+def test_zenithal_projection_cell_centres(proj):
+    """Reading R26: gnomonic (TAN) / orthographic (SIN) cell centres.  Closed forms with the
+    reference point at (0, 0): along the x axis lon = atan(x) (TAN) or asin(x) (SIN) with
+    lat = 0, along the y axis lat = atan(y) / asin(y); anywhere, the great-circle distance from
+    the reference point is atan(r) / asin(r) (r = the offset in radians); the reference
+    pixel is the reference point."""
+    f = math.atan if proj == "tan" else math.asin
+    m = {"nx": 21, "ny": 21, "crval_lon": 0.0, "crval_lat": 0.0, "crpix_x": 11.0, "crpix_y": 11.0,
+         "cdelt_lon": 1.5, "cdelt_lat": 1.5, "projection": proj}
+    for i in range(21):
+        x = (i + 1 - 11.0) * 1.5
+        lon, lat = oracle.cell_centre(m, i, 10)
+        assert abs(lon - math.degrees(f(math.radians(x)))) < 1e-12 and abs(lat) < 1e-12
+        lon, lat = oracle.cell_centre(m, 10, i)
+        assert abs(lat - math.degrees(f(math.radians(x)))) < 1e-12 and abs(lon) < 1e-12
+    m2 = dict(m, crval_lon=30.0, crval_lat=41.0, cdelt_lon=-0.7, cdelt_lat=0.4)
+    c0 = oracle.cell_centre(m2, 10, 10)
+    assert abs(c0[0] - 30.0) < 1e-12 and abs(c0[1] - 41.0) < 1e-12
+    for i, j in [(0, 0), (3, 17), (20, 5), (12, 9)]:
+        x, y = (i + 1 - 11.0) * -0.7, (j + 1 - 11.0) * 0.4
+        r = math.radians(math.hypot(x, y))
+        lon, lat = oracle.cell_centre(m2, i, j)
+        d = oracle.distance_deg(30.0, 41.0, lon, lat)
+        assert abs(d - math.degrees(f(r))) < 1e-10, (i, j, d)
+        # east (x > 0 with cdelt_lon < 0 means i left of crpix) -> the sign of the lon offset
+        assert (lon - 30.0) * x > 0 or abs(x) < 1e-12
