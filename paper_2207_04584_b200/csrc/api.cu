@@ -123,7 +123,16 @@ void phase_mark(const char* what) {
     static auto t0 = std::chrono::steady_clock::now();
     if (!on) return;
     const auto t = std::chrono::steady_clock::now();
-    fprintf(stderr, "[hegrid] %-32s %9.2f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    // with the device pool's reserved / used bytes (growing the pool maps new memory)
+    uint64_t res = 0, used = 0;
+    int dev = 0;
+    cudaMemPool_t pool = nullptr;
+    if (cudaGetDevice(&dev) == cudaSuccess && shared_pool(dev, &pool) == cudaSuccess) {
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    }
+    fprintf(stderr, "[hegrid] %-32s %9.2f ms  pool %.2f / %.2f GB\n", what,
+            std::chrono::duration<double, std::milli>(t - t0).count(), used / 1e9, res / 1e9);
     t0 = t;
 }
 

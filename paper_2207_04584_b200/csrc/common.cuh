@@ -178,6 +178,17 @@ inline cudaError_t plan_alloc(const hegrid_plan_s* p, void* ptr, size_t bytes, c
     return cudaMallocFromPoolAsync(reinterpret_cast<void**>(ptr), bytes, p->pool, st);
 }
 
+// stream-ordered scratch from the current device's pool (never trimmed, unlike the default
+// pool, which returns its memory at every synchronisation)
+inline cudaError_t scratch_alloc(void* ptr, size_t bytes, cudaStream_t st) {
+    int dev = 0;
+    cudaMemPool_t pool = nullptr;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = shared_pool(dev, &pool);
+    if (e != cudaSuccess) return e;
+    return cudaMallocFromPoolAsync(reinterpret_cast<void**>(ptr), bytes, pool, st);
+}
+
 inline hegrid_status cuda_status(cudaError_t e) {
     if (e == cudaSuccess) return HEGRID_OK;
     if (e == cudaErrorMemoryAllocation) return HEGRID_ENOMEM;

@@ -150,9 +150,9 @@ hegrid_status radix_sort_pairs(uint32_t* d_keys, int32_t* d_vals, int64_t n, int
     int64_t total = 256LL * ntiles;
     uint32_t *k2 = nullptr, *cnt = nullptr;
     int32_t* v2 = nullptr;
-    HG_TRY(cudaMallocAsync(&k2, n * sizeof(uint32_t), st));
-    HG_TRY(cudaMallocAsync(&v2, n * sizeof(int32_t), st));
-    HG_TRY(cudaMallocAsync(&cnt, total * sizeof(uint32_t), st));
+    HG_TRY(scratch_alloc(&k2, n * sizeof(uint32_t), st));
+    HG_TRY(scratch_alloc(&v2, n * sizeof(int32_t), st));
+    HG_TRY(scratch_alloc(&cnt, total * sizeof(uint32_t), st));
     uint32_t *ka = d_keys, *kb = k2;
     int32_t *va = d_vals, *vb = v2;
     int passes = (bits + 7) / 8;
@@ -310,6 +310,7 @@ hegrid_status build_plan(hegrid_plan_s* p, const double* d_lon, const double* d_
     std::vector<int> mrow;
     std::vector<float> cos_row;
     HG_TRY_S(make_geom(p, mrow, cos_row));
+    phase_mark("build: geometry");
     const Geom& g = p->g;
     int64_t n = p->n;
     cudaEvent_t e0, e1;
@@ -327,8 +328,9 @@ hegrid_status build_plan(hegrid_plan_s* p, const double* d_lon, const double* d_
     HG_TRY(cudaMemcpyAsync(p->d_mrow, mrow.data(), g.nrow * sizeof(int), cudaMemcpyHostToDevice, st));
     HG_TRY(cudaMemcpyAsync(p->d_cos_row, cos_row.data(), g.ny * sizeof(float),
                            cudaMemcpyHostToDevice, st));
+    phase_mark("build: allocations");
     int* d_bad = nullptr;
-    HG_TRY(cudaMallocAsync(&d_bad, sizeof(int), st));
+    HG_TRY(plan_alloc(p, &d_bad, sizeof(int), st));
     HG_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
     // device time of the plan kernels only (allocations above are not part of it)
     HG_TRY(cudaEventRecord(e0, st));
@@ -348,7 +350,7 @@ hegrid_status build_plan(hegrid_plan_s* p, const double* d_lon, const double* d_
     count_launch();
     HG_TRY(cudaGetLastError());
     unsigned long long* d_mx = nullptr;
-    HG_TRY(cudaMallocAsync(&d_mx, sizeof(unsigned long long), st));
+    HG_TRY(plan_alloc(p, &d_mx, sizeof(unsigned long long), st));
     HG_TRY(cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long), st));
     {
         int64_t cells = (int64_t)g.nx * g.ny;
@@ -366,7 +368,9 @@ hegrid_status build_plan(hegrid_plan_s* p, const double* d_lon, const double* d_
     HG_TRY(cudaMemcpyAsync(&used, p->d_bin_start + g.nbins, sizeof(uint32_t),
                            cudaMemcpyDeviceToHost, st));
     HG_TRY(cudaFreeAsync(d_bad, st));
+    phase_mark("build: enqueued");
     HG_TRY(cudaStreamSynchronize(st));
+    phase_mark("build: synchronised");
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);
