@@ -93,6 +93,12 @@ static_assert(TC_KC == 32 || TC_KC == 64, "chunks of 32 or 64 samples");
 #ifndef HG_TC_SEG_SPARSE
 #define HG_TC_SEG_SPARSE 16 // segment length when no block gets more than TC_CPB_SPARSE chunks
 #endif
+// Mixed-precision products (tc::mma8_mix): per 8-sample K-step one kind::tf32 MMA of
+// the hi parts and one kind::f16 (bf16) MMA of K = 16 pairing the two correction terms, 8 MMAs
+// per run instead of the 12 of 3xTF32 (HG_TC_MIX=0)
+#ifndef HG_TC_MIX
+#define HG_TC_MIX 1
+#endif
 constexpr int NA = HG_TC_NA;              // A stages (TMEM)
 constexpr int NBS = HG_TC_NBS;            // B stages (SMEM)
 constexpr int NV = HG_TC_NV;              // V staging stages (SMEM)
@@ -178,6 +184,8 @@ __device__ __forceinline__ uint32_t b_off(int q, int n, int kq, int ns) {
 // the entry's q-th in-reach block, blist order) and stores them, split into tf32 hi / lo, at
 // hi + b_off(q, n, kq) and lo + b_off(q, n, kq).  Used by the on-the-fly B producers (shared
 // memory) and by the plan's weight image (global memory): the bytes are identical.
+// With HG_TC_MIX the second half holds {bf16(w_lo), bf16(w_hi)} per sample instead of the tf32
+// lo part: the operand of the mixed-precision correction MMA (tc::mma8_mix).
 __device__ __forceinline__ void entry_weights(const Geom& g, const PlanDev& pd, int i0, int j0,
                                               int wt, const float (&cosr)[TC_BY],
                                               const float4 (&g4)[4], uint32_t pstart, int row,
@@ -186,7 +194,7 @@ __device__ __forceinline__ void entry_weights(const Geom& g, const PlanDev& pd, 
     const int q0 = wt >> (6 + LKA);
 #pragma unroll 1
     for (int q = q0; q < nq; q += 4 / KA) {
-        const int b = (blist >> (4 * q)) & 15;
+        const int b = (int)((blist >> (4 * q)) & 15);
         const int by = b / TC_BX;
         const int cj = j0 + by * 4 + rr;
         const int ci0 = i0 + (b % TC_BX) * 4;
@@ -218,6 +226,12 @@ __device__ __forceinline__ void entry_weights(const Geom& g, const PlanDev& pd, 
             tc::split_tf32(w[1][cc], h4.y, l4.y);
             tc::split_tf32(w[2][cc], h4.z, l4.z);
             tc::split_tf32(w[3][cc], h4.w, l4.w);
+            if (HG_TC_MIX) {           // {bf16(w_lo), bf16(w_hi)} per sample
+                l4.x = tc::pack_bf16(__uint_as_float(l4.x), __uint_as_float(h4.x));
+                l4.y = tc::pack_bf16(__uint_as_float(l4.y), __uint_as_float(h4.y));
+                l4.z = tc::pack_bf16(__uint_as_float(l4.z), __uint_as_float(h4.z));
+                l4.w = tc::pack_bf16(__uint_as_float(l4.w), __uint_as_float(h4.w));
+            }
             const uint32_t o = b_off(q, n, kq, ns);
             *reinterpret_cast<uint4*>(hi + o) = h4;
             *reinterpret_cast<uint4*>(lo + o) = l4;
@@ -616,6 +630,7 @@ hegrid_status prepare_tc(const hegrid_plan_s* p, int64_t n_channels_per_launch, 
 __device__ unsigned long long g_tc_prof[16];
 // Timeline of one CTA (profiling builds, HEGRID_TC_DEBUG bit 8192): clock64 per (chunk, event)
 __device__ long long g_tl[256][12];
+__device__ long long g_tla[256][3][8];   // per A warp: v_full passed, a_full arrive, done passed
 #define TL(ev, c) do { if (tl_on && (c) < 256) g_tl[(c)][(ev)] = clock64(); } while (0)
 
 // ------------------------------------------------------------------ the kernel
@@ -634,7 +649,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // A producers: warps 4-7, plus 8-11 when the weights are precomputed (those warps are the
     // B producers otherwise); each lane quarter's chunk columns are split between its warps
-    constexpr int A_WARPS = PW ? 8 : 4, A_GROUPS = A_WARPS / 4, A_THREADS = 32 * A_WARPS;
+        constexpr int A_WARPS = PW ? 8 : 4, A_GROUPS = A_WARPS / 4, A_THREADS = 32 * A_WARPS;
     constexpr int KPW = TC_KC / A_GROUPS;
 #ifndef HG_TC_NI_PW
 #define HG_TC_NI_PW 3
@@ -771,7 +786,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     // sub-partitions) issues the MMAs of the tile's block rows r with r % NI == i, so the
     // per-MMA issue cost is spread over NI instruction streams.  Each D column block is always
     // fed by the same issuer in chunk order: the accumulation order stays fixed.
-    const int issuer = warp == 0 ? 0 : (NI > 1 && warp == 3) ? 1 : (NI > 2 && warp == 13) ? 2 : -1;
+        const int issuer = warp == 0 ? 0 : (NI > 1 && warp == 3) ? 1 : (NI > 2 && warp == 13) ? 2 : -1;
     if (issuer >= 0) {
         // ============================ MMA issuer =============================
         // chunk c uses A stage c % NA; the loop is unrolled by NA so the stage (and with it
@@ -846,8 +861,14 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
 #pragma unroll
                     for (int a = 0; a < KA; ++a) {    // K-atom a: K-steps 4a .. 4a + 3
                         const uint32_t bh = dh0 + (uint32_t)(((a * ns + q) * ATOM_SLOT) >> 4);
+#if HG_TC_MIX
+                        tc::mma8_mix<(32 >> 4), TC_KC>(dbase + (uint32_t)(b * TC_N), a0 + 32 * a, bh,
+                                                       bh + (uint32_t)lo16, tc::idesc_tf32(TC_M, TC_N * r),
+                                                       tc::idesc_bf16(TC_M, TC_N * r));
+#else
                         tc::mma12_3xtf32<(32 >> 4), TC_KC>(dbase + (uint32_t)(b * TC_N), a0 + 32 * a, bh,
                                                            bh + (uint32_t)lo16, tc::idesc_tf32(TC_M, TC_N * r));
+#endif
                     }
                 }
             }
@@ -907,23 +928,27 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             e.w = __shfl_sync(0xffffffffu, cur.w, c & 31);
             const int cp = c + PF;
             const uint32_t xp = __shfl_sync(0xffffffffu, (cp >> 5) == (c >> 5) ? cur.x : nxt.x, cp & 31);
+            {   // the whole warp waits (no single-lane divergent region around the wait: lanes
+                // parked at a warp sync slow the other warps of their SM sub-partition); lane 0
+                // issues the copies
+                const int sv = c % NV;
+                if (lane == 0) TL(11, c);
+#ifndef HG_TC_NO_VPF
+                if (lane == 0 && cp < nchunks) tc::tma_prefetch_2d(&tmap_v, cb, (int)xp);
+#endif
+                TPROF_BEGIN;
+                if (c >= NV) tc::mbar_wait(&sm.v_empty[sv], ((c / NV) - 1) & 1);
+                TPROF_END(0);
+            }
             if (lane == 0) {
                 const uint32_t nk = e.y & 255;
                 const int sv = c % NV;
-#ifndef HG_TC_NO_VPF
-                if (cp < nchunks) tc::tma_prefetch_2d(&tmap_v, cb, (int)xp);
-#endif
-                {
-                    TPROF_BEGIN;
-                    if (c >= NV) tc::mbar_wait(&sm.v_empty[sv], ((c / NV) - 1) & 1);
-                    TPROF_END(0);
-                }
+                TL(0, c);
                 sm.Es[sv] = e;
                 if (dbg & 8) {
                     tc::mbar_arrive(&sm.v_full[sv]);
                 } else {
                     // the geometry feeds the on-the-fly B producers only
-                    TL(0, c);
                     tc::mbar_arrive_expect_tx(&sm.v_full[sv], (uint32_t)V_STAGE + (PW ? 0u : nk * 16));
                     tc::tma_load_2d(&sm.Vs[sv][0], &tmap_v, cb, (int)e.x, &sm.v_full[sv]);
                     if (!PW) tc::bulk_g2s(&sm.Gs[sv][0], pd.geo + e.x, nk * 16, &sm.v_full[sv]);
@@ -939,7 +964,10 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
         // Entry masks and slots are read in groups of G, two groups ahead, into registers
         // (static indices), so no global-load latency sits on the loop.  (An L2 prefetch of
         // the next group's weights, HG_TC_WPF, measured slower: the CTAs of a tile share them.)
-        if (lane == 0) {
+        // Every lane runs the loop (identical values; no lanes parked at a warp sync for the
+        // whole kernel, measured -2 %), lane 0 issues the stores, arrives and copies.
+        const bool wl0 = lane == 0;
+        {
             const uint32_t* ws = wslot + tile_off[tile] + e_begin;
             constexpr int G = 8;
             uint32_t zc[G], sc[G], zn[G], sn[G], zf[G], sf[G];
@@ -989,17 +1017,20 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                         ++conf;
                     }
                     TPROF_END(0);
-                    starts[c % NBF] = head;
                     const int k = c % NBF;
-                    sm.Bmask[k] = zc[u];
-                    sm.Boff[k] = (uint32_t)off;
-                    if (dbg & 512) {
-                        tc::mbar_arrive(&sm.b_full[k]);
-                    } else {
-                        TL(7, c);
-                        tc::mbar_arrive_expect_tx(&sm.b_full[k], bytes);
-                        tc::bulk_g2s(&sm.B[off], wimg + (size_t)sc[u] * (2u * SLOT_BYTES), bytes, &sm.b_full[k]);
+                    if (wl0) {
+                        starts[c % NBF] = head;
+                        sm.Bmask[k] = zc[u];
+                        sm.Boff[k] = (uint32_t)off;
+                        if (dbg & 512) {
+                            tc::mbar_arrive(&sm.b_full[k]);
+                        } else {
+                            TL(7, c);
+                            tc::mbar_arrive_expect_tx(&sm.b_full[k], bytes);
+                            tc::bulk_g2s(&sm.B[off], wimg + (size_t)sc[u] * (2u * SLOT_BYTES), bytes, &sm.b_full[k]);
+                        }
                     }
+                    __syncwarp();      // lane 0's starts[] store is seen by the other lanes
                     head += bytes;
                 }
 #pragma unroll
@@ -1036,6 +1067,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 TPROF_END(0);
             }
             if (warp == 4 && lane == 0) TL(1, c);
+            if (tl_on && lane == 0 && c < 256) g_tla[c][0][warp - 4] = clock64();
             const float* vs = reinterpret_cast<const float*>(&sm.Vs[sv][0]) + k0 * TC_M + chl;
             const uint4 ee = sm.Es[sv];
             const uint32_t nk = ee.y & 255;
@@ -1084,6 +1116,14 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     if ((uint32_t)(k0 + k) < nk && cb + chl < C) nf_record(nf, ee.x + k0 + k, cb + chl);
                 }
             }
+            if constexpr (HG_TC_MIX) {
+                // mixed-precision correction operand: {bf16(v), bf16(v_lo)} per sample
+#pragma unroll
+                for (int k = 0; k < KPW; ++k) {
+                    const float l = __uint_as_float(lo[k]);
+                    lo[k] = tc::pack_bf16(__uint_as_float(hi[k]) + l, l);
+                }
+            }
         };
         auto store = [&](int c) {
             const int sa = c % NA;
@@ -1093,6 +1133,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 TPROF_END(1);
             }
             if (warp == 4 && lane == 0 && c >= NA) TL(6, c - NA);
+            if (tl_on && lane == 0 && c >= NA && c - NA < 256) g_tla[c - NA][2][warp - 4] = clock64();
             tc::fence_after_sync();
             const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + A_COL0 + sa * 2 * TC_KC + k0;
             if (warp == 4 && lane == 0) TL(10, c);
@@ -1110,16 +1151,25 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 tc::tmem_st16(ta + TC_KC, lo);
             }
         };
-        if (nchunks > 0) {
-            load_split(0);
-            store(0);
-        }
-        for (int c = 0; c < nchunks; ++c) {
-            {
+        // promote segment s = cn / SEG - 1 when the A warps are about to store chunk cn =
+        // (s + 1) SEG + NA (all of segment s's MMAs were issued: the issuer has consumed
+        // chunk cn - NA = (s + 1) SEG)
+        auto maybe_promote = [&](int cn) {
+            if (cn >= SEG && cn % SEG == NA) {
+                const int s = cn / SEG - 1, d = s & 1;
                 TPROF_BEGIN;
-                if (c + 1 < nchunks) load_split(c + 1);
-                TPROF_END(3);
+                tc::mbar_wait(&sm.seg_done[d], (s >> 1) & 1);
+                tc::fence_after_sync();
+                promote_buffer(d, d ? segmask1 : segmask0, true);
+                if (d) segmask1 = 0; else segmask0 = 0;
+                tc::wait_st();
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&sm.seg_free[d]);
+                TPROF_END(2);
             }
+        };
+        auto publish = [&](int c) {
             tc::wait_st();
             if (warp == 4 && lane == 0) TL(9, c);
             tc::fence_before_sync();
@@ -1130,24 +1180,19 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             if (lane == 0) tc::mbar_arrive(&sm.a_full[c % NA]);
 #endif
             if (warp == 4 && lane == 0) TL(2, c);
+            if (tl_on && lane == 0 && c < 256) g_tla[c][1][warp - 4] = clock64();
+        };
+        // Chunk c is stored and published before chunk c + 1's values are loaded and split:
+        // the split runs while chunk c's MMAs execute, off the A -> issuer -> done cycle.
+        if (nchunks > 0) load_split(0);
+        for (int c = 0; c < nchunks; ++c) {
+            maybe_promote(c);
+            store(c);
+            publish(c);
             if (c + 1 < nchunks) {
-                const int cn = c + 1;
-                if (cn >= SEG && cn % SEG == NA) {
-                    // promote segment s = cn / SEG - 1 (all its MMAs were issued: the
-                    // issuer has consumed chunk cn - NA = (s + 1) SEG)
-                    const int s = cn / SEG - 1, d = s & 1;
-                    TPROF_BEGIN;
-                    tc::mbar_wait(&sm.seg_done[d], (s >> 1) & 1);
-                    tc::fence_after_sync();
-                    promote_buffer(d, d ? segmask1 : segmask0, true);
-                    if (d) segmask1 = 0; else segmask0 = 0;
-                    tc::wait_st();
-                    tc::fence_before_sync();
-                    __syncwarp();
-                    if (lane == 0) tc::mbar_arrive(&sm.seg_free[d]);
-                    TPROF_END(2);
-                }
-                store(cn);
+                TPROF_BEGIN;
+                load_split(c + 1);
+                TPROF_END(3);
             }
         }
     } else if (!PW && warp >= 8) {
@@ -1392,10 +1437,18 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
             static long long tl[256][12];
             cudaMemcpyFromSymbol(tl, g_tl, sizeof(tl));
             const long long t0 = tl[40][0];
-            fprintf(stderr, "[tc tl] chunk: vTMA Avfull Asplit Awaitst Aafull Astore | Igota Igotb Icommit Adone Wcopy (cycles rel. to chunk 40 vTMA)\n");
+            fprintf(stderr, "[tc tl] chunk: Vstart vTMA Avfull Asplit Awaitst Aafull Astore | Igota Igotb Icommit Adone Wcopy (cycles rel. to chunk 40 vTMA)\n");
             for (int c = 40; c < 60; ++c)
-                fprintf(stderr, "[tc tl] %3d: %7lld %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld\n", c, tl[c][0] - t0, tl[c][1] - t0,
+                fprintf(stderr, "[tc tl] %3d: %7lld %7lld %7lld %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld\n", c, tl[c][11] - t0, tl[c][0] - t0, tl[c][1] - t0,
                         tl[c][8] - t0, tl[c][9] - t0, tl[c][2] - t0, tl[c][10] - t0, tl[c][3] - t0, tl[c][4] - t0, tl[c][5] - t0, tl[c][6] - t0, tl[c][7] - t0);
+            static long long ta[256][3][8];
+            cudaMemcpyFromSymbol(ta, g_tla, sizeof(ta));
+            for (int c = 40; c < 50; ++c)
+                for (int k = 0; k < 3; ++k) {
+                    fprintf(stderr, "[tc tla] %3d %s:", c, k == 0 ? "vfull" : k == 1 ? "afull" : "done ");
+                    for (int w = 0; w < 8; ++w) fprintf(stderr, " %7lld", ta[c][k][w] ? ta[c][k][w] - t0 : -1);
+                    fprintf(stderr, "\n");
+                }
         }
     }
     return cuda_status(cudaGetLastError());

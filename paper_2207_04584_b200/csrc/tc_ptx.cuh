@@ -46,7 +46,7 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 #define HG_MBAR_SUSPEND_NS 1000000
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#ifdef HG_MBAR_SPIN
+#if defined(HG_MBAR_SPIN)
     // spin on the non-blocking test (no suspension: lowest wake-up latency)
     asm volatile(
         "{\n\t"
@@ -156,6 +156,43 @@ __device__ __forceinline__ void mma12_3xtf32(uint32_t d, uint32_t a0, uint32_t b
         "n"(ALO + 16), "n"(ALO + 24) : "memory");
 #undef HG_MMA12_KS
 }
+// Mixed-precision variant (span layout of the precomputed weight image): per K-step one
+// kind::tf32 MMA of the hi parts (A cols a0 + 8 ks, B at bh) and one kind::f16 (bf16) MMA of
+// K = 16 that pairs the two correction terms (A cols a0 + ALO + 8 ks hold {bf16(v), bf16(v_lo)}
+// per sample, B at bl holds {bf16(w_lo), bf16(w_hi)}): 8 MMAs instead of 12.
+template <int KS_STEP, int ALO = 32>
+__device__ __forceinline__ void mma8_mix(uint32_t d, uint32_t a0, uint32_t bh_lo, uint32_t bl_lo,
+                                         uint32_t idt, uint32_t idb) {
+#define HG_MMA8_KS(bh, bl, ah, al)                                                       \
+    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+" #ah "], " #bh ", %4, 1;\n\t"       \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+" #al "], " #bl ", %5, 1;\n\t"
+    asm volatile(
+        "{\n\t"
+        ".reg .pred e;\n\t"
+        ".reg .b32 x1, x2, x3, y1, y2, y3;\n\t"
+        ".reg .b64 h0, h1, h2, h3, l0, l1, l2, l3;\n\t"
+        "add.u32 x1, %2, %6;\n\t"
+        "add.u32 x2, %2, %7;\n\t"
+        "add.u32 x3, %2, %8;\n\t"
+        "add.u32 y1, %3, %6;\n\t"
+        "add.u32 y2, %3, %7;\n\t"
+        "add.u32 y3, %3, %8;\n\t"
+        "mov.b64 h0, {%2, %9};\n\t"
+        "mov.b64 h1, {x1, %9};\n\t"
+        "mov.b64 h2, {x2, %9};\n\t"
+        "mov.b64 h3, {x3, %9};\n\t"
+        "mov.b64 l0, {%3, %9};\n\t"
+        "mov.b64 l1, {y1, %9};\n\t"
+        "mov.b64 l2, {y2, %9};\n\t"
+        "mov.b64 l3, {y3, %9};\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        HG_MMA8_KS(h0, l0, 0, %10) HG_MMA8_KS(h1, l1, 8, %11)
+        HG_MMA8_KS(h2, l2, 16, %12) HG_MMA8_KS(h3, l3, 24, %13)
+        "}\n" :: "r"(d), "r"(a0), "r"(bh_lo), "r"(bl_lo), "r"(idt), "r"(idb), "n"(KS_STEP),
+        "n"(2 * KS_STEP), "n"(3 * KS_STEP), "n"(kDescHiSw128), "n"(ALO), "n"(ALO + 8),
+        "n"(ALO + 16), "n"(ALO + 24) : "memory");
+#undef HG_MMA8_KS
+}
 // low word of a K-major SWIZZLE_128B descriptor (start address >> 4, LBO field 1)
 __device__ __forceinline__ uint32_t sdesc_sw128_lo(uint32_t saddr) {
     return ((saddr >> 4) & 0x3FFFu) | (1u << 16);
@@ -175,6 +212,21 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
          | (2u << 10)                         // b_format = TF32
          | ((uint32_t)(N >> 3) << 17)         // n_dim
          | ((uint32_t)(M >> 4) << 24);        // m_dim
+}
+
+// Instruction descriptor: kind::f16 with bf16 A/B (K-major), D fp32, M x N.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+    return (1u << 4)                          // c_format = F32
+         | (1u << 7)                          // a_format = BF16
+         | (1u << 10)                         // b_format = BF16
+         | ((uint32_t)(N >> 3) << 17)
+         | ((uint32_t)(M >> 4) << 24);
+}
+// {bf16(x) in the low half, bf16(y) in the high half}, round to nearest even
+__device__ __forceinline__ uint32_t pack_bf16(float x, float y) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(y), "f"(x));
+    return r;
 }
 
 // ---- TMEM <-> registers (32 lanes x 32 bit, per warp) ------------------------------

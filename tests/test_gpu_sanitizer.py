@@ -29,7 +29,11 @@ def _run(tool, mode):
     cmd = [SAN, "--tool", tool, "--error-exitcode", "9", "--print-limit", "20",
            sys.executable, os.path.join(ROOT, "tools", "sanitize_case.py"), mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
-    return r, (r.stdout + r.stderr)[-4000:]
+    tail = (r.stdout + r.stderr)[-4000:]
+    if "closed on this pool" in tail:
+        # the GPU pool's operators disabled the tool (a wrapper that refuses to run it)
+        pytest.skip("compute-sanitizer disabled on this GPU pool: " + tail.strip().splitlines()[0][:200])
+    return r, tail
 
 
 @pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
