@@ -110,7 +110,7 @@ typedef struct hegrid_kernel {
 typedef enum hegrid_engine {
     HEGRID_ENGINE_AUTO = 0,   /* library picks (currently the tensor-core engine) */
     HEGRID_ENGINE_SIMT = 1,   /* FP32 SIMT accumulate (register-blocked, lanes own channels) */
-    HEGRID_ENGINE_TC = 2      /* tcgen05 tensor cores, 3xTF32 error-compensated (fp32-accurate) */
+    HEGRID_ENGINE_TC = 2      /* tcgen05 tensor cores, error-compensated (fp32-accurate): tf32 hi*hi + bf16 corrections */
 } hegrid_engine;
 
 /* Optional knobs; pass NULL for defaults. */
