@@ -1366,14 +1366,16 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     int C = (int)n_channels;
     int tiles = ((g.nx + TC_TW - 1) / TC_TW) * ((g.ny + TC_TH - 1) / TC_TH);
     const int ncb = (C + TC_M - 1) / TC_M;
-    // split the tiles' entry lists when the grid would leave SMs idle: about four waves
+    // split the tiles' entry lists when the grid would leave SMs idle: about eight waves of
+    // CTAs (finer parts balance the uneven per-tile work; cfg3: 14 parts 3.98 ms, 7 parts 4.14,
+    // 5 parts 4.30, tools/split_sweep.sh)
     int nsplit = 1;
     {
         int nsm = 148;
         int dev = 0;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         const int64_t ctas = (int64_t)tiles * ncb;
-        if (ctas < 2 * nsm) nsplit = (int)std::min<int64_t>(8, std::max<int64_t>(1, (4 * nsm + ctas / 2) / ctas));
+        if (ctas < 2 * nsm) nsplit = (int)std::min<int64_t>(16, std::max<int64_t>(1, (8 * nsm + ctas - 1) / ctas));
         if (const char* e = getenv("HEGRID_TC_SPLIT")) nsplit = std::max(1, std::min(16, atoi(e)));
     }
     dim3 grid(tiles * ncb * nsplit);
