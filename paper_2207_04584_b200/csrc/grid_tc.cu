@@ -1,5 +1,5 @@
-// grid_tc.cu -- accumulate + normalise on the 5th-gen tensor cores (tcgen05, kind::tf32),
-// error-compensated 3xTF32 so the sums keep fp32 accuracy.
+// grid_tc.cu -- accumulate + normalise on the 5th-gen tensor cores (tcgen05: kind::tf32 and
+// kind::f16), error-compensated so the sums keep fp32 accuracy.
 //
 // The contraction (Eq. 1 numerator): S[c][cell] = sum_n v[c][n] w(cell,n).
 // Blocked: for a chunk of K = 32 plan-ordered candidate samples of one bin row and a run
@@ -8,8 +8,11 @@
 // with A = the chunk's values (channels on TMEM lanes), B = the (cell, sample) weights
 // computed by the CTA's SIMT warps (each weight once per CTA, shared by its 128 channels:
 // the paper's component-share principle), D = fp32 accumulators in TMEM.
-// Each operand is split x = hi + lo (tc::split_tf32); three MMAs (hi*hi + hi*lo + lo*hi)
-// reproduce the fp32 product to ~2^-21.
+// Each operand is split x = hi + lo (tc::split_tf32, hi = x rounded to tf32, lo exact); per
+// 8-sample K-step one kind::tf32 MMA multiplies the hi parts (exact in fp32) and one kind::f16
+// MMA of K = 16 adds both correction terms, bf16(v) bf16(w_lo) + bf16(v_lo) bf16(w_hi)
+// (tc::mma8_mix): the fp32 product to <= 2^-17 (RMS 2^-20.6) with 8 MMAs per run (the
+// 3xTF32 scheme hi*hi + hi*lo + lo*hi, ~2^-21 with 12 MMAs, with -DHG_TC_MIX=0).
 //
 // Shared per plan (built on first use, reused by every launch and channel block):
 //   * the per-tile chunk schedule {plan position, n, bin row, mask of reachable blocks}
@@ -20,12 +23,14 @@
 // k_accum_tc: CTA = 16x12 cells (12 blocks of 4x4) x 128 channels, 512 threads in roles:
 //   MMA issuers (warps 0, 3, and 13 with precomputed weights): issuer i issues the MMAs of
 //                     the block rows r with r % NI == i: per run of consecutive in-reach
-//                     blocks, 4 K-steps x 3 products (N = 16 r), one commit per chunk;
+//                     blocks, 4 K-steps x 2 MMAs (N = 16 r), one commit per chunk;
 //   warp 1          : value loader: one 2D TMA box (32 plan rows x 128 channels) per chunk
 //                     into a 3-stage ring (+ the chunk's geometry in on-the-fly mode);
 //   warp 2 (PW)     : weight loader: the chunk's precomputed weight-image bytes into a ring;
-//   A producers     : (thread = channel = TMEM lane) split the staged values into tf32 hi/lo
-//                     and tcgen05.st them into one of 2 TMEM A stages; every SEG chunks they
+//   A producers     : (thread = channel = TMEM lane) split the staged values into the tf32
+//                     hi part and the packed bf16 correction operand and tcgen05.st them into
+//                     one of 2 TMEM A stages, publishing each chunk before splitting the
+//                     next one; every SEG chunks they
 //                     add the finished D buffer into the fp32 master tile in shared memory
 //                     (D is double-buffered in TMEM, round-to-nearest promotion bounds the
 //                     tensor core's truncating accumulation);
