@@ -1397,12 +1397,19 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     int want_pw = ncb >= (int)TC_PW_MIN_CBLOCKS;
     if (const char* e = getenv("HEGRID_TC_PW")) want_pw = atoi(e);
     const bool pw = want_pw && ensure_tc_wimage(p, st);
-    // channel-block group: all blocks of a tile together when the weights are precomputed (their
-    // entries are then read from HBM about once), tile-major otherwise (values of neighbouring
-    // tiles shared in L2); HEGRID_TC_GROUP overrides
-    int cgroup = pw ? ncb : 1;
+    // CTA walk (DRAM traffic, not time: the kernel does not wait on DRAM; tools/order_sweep.sh,
+    // cfg4): with precomputed weights, groups of 8 channel blocks of a tile run together (the
+    // tile's weight entries are read ~4x from HBM instead of 32x), tiles in 3 x 3 super-tiles,
+    // odd tile rows walking their entries backwards, so tiles resident together share their
+    // candidate samples in L2: 34.4 GB per cfg4 launch against 38.1 GB with all 32 channel
+    // blocks of a tile together and row-major tiles (75 GB tile-major, group 1).  On-the-fly
+    // weights: tile-major.  Few channel blocks (cfg2, cfg3): row-major tiles, measured faster
+    // there.  The snake changes a tile's accumulation order, so it depends on the channel count
+    // only (both weight modes give bit-identical maps).  HEGRID_TC_GROUP / _SUPER / _SNAKE
+    // override.
+    int cgroup = pw ? std::min(ncb, 8) : 1;
     if (const char* e = getenv("HEGRID_TC_GROUP")) cgroup = std::max(1, std::min(ncb, atoi(e)));
-    int super_ = 1, snake = 0;
+    int super_ = pw && ncb >= 8 ? 3 : 1, snake = ncb >= 8 ? 1 : 0;
     if (const char* e = getenv("HEGRID_TC_SUPER")) super_ = std::max(1, atoi(e));
     if (const char* e = getenv("HEGRID_TC_SNAKE")) snake = atoi(e);
     NfBuf nf;
