@@ -86,8 +86,11 @@ static_assert(TC_KC == 32 || TC_KC == 64, "chunks of 32 or 64 samples");
 // fp32 master tile in shared memory, 3 or more stages no longer fit the 227 KB budget, so
 // the question is moot for this kernel.  NBS = 2 is bit-deterministic run to run:
 // tools/det_otf.sh, profiles/r2/det_otf_nbs.log.)
+#ifndef HG_TC_MAXQ
+#define HG_TC_MAXQ 8
+#endif
 #ifndef HG_TC_NBS
-#define HG_TC_NBS 2
+#define HG_TC_NBS (HG_TC_MAXQ > 8 ? 1 : 2)
 #endif
 #ifndef HG_TC_NV
 #define HG_TC_NV 3
@@ -107,7 +110,11 @@ static_assert(TC_KC == 32 || TC_KC == 64, "chunks of 32 or 64 samples");
 constexpr int NA = HG_TC_NA;              // A stages (TMEM)
 constexpr int NBS = HG_TC_NBS;            // B stages (SMEM)
 constexpr int NV = HG_TC_NV;              // V staging stages (SMEM)
-constexpr int MAXQ = 8;                   // max blocks (B slots) per chunk entry
+// max blocks (B slots) per schedule entry (a chunk reaching more gets two entries, 7 % of
+// cfg4's chunks).  12 (every block of the tile, one entry per chunk, one 48 KB on-the-fly
+// weight stage) measured cfg4 12.89 vs 12.97 ms but cfg3 4.08 vs 3.99 ms and OTF cfg3 8.85 vs
+// 8.2 ms, so 8.
+constexpr int MAXQ = HG_TC_MAXQ;
 // The tensor core's fp32 accumulation truncates, so its error grows with the number of MMAs
 // accumulated into one D element.  D is therefore double-buffered in TMEM by segments of
 // SEG chunks: while the tensor core accumulates segment s+1 into one buffer, the A warps add
@@ -186,7 +193,7 @@ __device__ __forceinline__ uint32_t b_off(int q, int n, int kq, int ns) {
 
 // The B operand of one chunk entry: thread wt (0..255) of the B-producer group computes its
 // (sample quad kq, column pair ch2, cell row rr) items of slots q0 = wt >> 6, q0 + 4 (slot q =
-// the entry's q-th in-reach block, blist order) and stores them, split into tf32 hi / lo, at
+// the entry's q-th in-reach block in mask order) and stores them, split into tf32 hi / lo, at
 // hi + b_off(q, n, kq) and lo + b_off(q, n, kq).  Used by the on-the-fly B producers (shared
 // memory) and by the plan's weight image (global memory): the bytes are identical.
 // With HG_TC_MIX the second half holds {bf16(w_lo), bf16(w_hi)} per sample instead of the tf32
@@ -194,12 +201,12 @@ __device__ __forceinline__ uint32_t b_off(int q, int n, int kq, int ns) {
 __device__ __forceinline__ void entry_weights(const Geom& g, const PlanDev& pd, int i0, int j0,
                                               int wt, const float (&cosr)[TC_BY],
                                               const float4 (&g4)[4], uint32_t pstart, int row,
-                                              uint32_t blist, int nq, int ns, uint8_t* hi, uint8_t* lo) {
+                                              uint32_t mask, int nq, int ns, uint8_t* hi, uint8_t* lo) {
     const int kq = wt & (8 * KA - 1), ch2 = (wt >> (3 + LKA)) & 1, rr = (wt >> (4 + LKA)) & 3;
     const int q0 = wt >> (6 + LKA);
 #pragma unroll 1
     for (int q = q0; q < nq; q += 4 / KA) {
-        const int b = (int)((blist >> (4 * q)) & 15);
+        const int b = (int)__fns(mask, 0, q + 1);      // the q-th set bit of the mask
         const int by = b / TC_BX;
         const int cj = j0 + by * 4 + rr;
         const int ci0 = i0 + (b % TC_BX) * 4;
@@ -276,7 +283,7 @@ __device__ __forceinline__ bool block_reachable(const Geom& g, int bi, int bj, d
 }
 
 // Chunk schedule: one warp per tile; lanes evaluate 32 consecutive chunks of a row at once.
-// Entry = {plan position, n | bin row << 8, block mask, block list (4-bit nibbles, mask order)}.
+// Entry = {plan position, n | bin row << 8, block mask, 0}.
 // n_out != nullptr: count only; otherwise write entries at off[tile].
 __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int tiles,
                               uint32_t* __restrict__ n_out, const uint32_t* __restrict__ off,
@@ -345,13 +352,12 @@ __global__ void k_tc_schedule(const __grid_constant__ Geom g, PlanDev pd, int ti
                 uint32_t pos = base + cnt + incl - ne;
                 uint32_t rest = mk;
                 while (rest) {
-                    uint32_t part = 0, list = 0;
+                    uint32_t part = 0;
                     for (int k = 0; k < MAXQ && rest; ++k) {
-                        list |= (uint32_t)(__ffs(rest) - 1) << (4 * k);
                         part |= rest & (~rest + 1u);
                         rest &= rest - 1;
                     }
-                    sched[pos++] = make_uint4(p, n | ((uint32_t)br << 8), part, list);
+                    sched[pos++] = make_uint4(p, n | ((uint32_t)br << 8), part, 0u);
                 }
             }
             cnt += tot;
@@ -429,7 +435,7 @@ k_tc_pairs(const __grid_constant__ Geom g, PlanDev pd, const int32_t* __restrict
         const int row = (int)(e.y >> 8), nq = __popc(e.z);
         for (int it = threadIdx.x; it < nq * 4 * (TC_KC / 4); it += blockDim.x) {
             const int kq = it % (TC_KC / 4), rr = (it / (TC_KC / 4)) & 3, q = it / TC_KC;
-            const int b = (e.w >> (4 * q)) & 15;
+            const int b = (int)__fns(e.z, 0, q + 1);
             const int cj = j0 + (b / TC_BX) * 4 + rr, ci0 = i0 + (b % TC_BX) * 4;
             if (cj >= g.ny) continue;
             float4 s[4];
@@ -475,7 +481,7 @@ k_tc_wimage(const __grid_constant__ Geom g, PlanDev pd, const uint4* __restrict_
             g4[u] = (uint32_t)(4 * kq + u) < nk ? __ldg(&pd.geo[pstart + 4 * kq + u])
                                                 : make_float4(0.0f, kInvalidDy, 0.0f, 0.0f);
         uint8_t* hi = wimg + (size_t)__ldg(&wslot[ei]) * (2u * SLOT_BYTES);
-        entry_weights(g, pd, i0, j0, wt, cosr, g4, pstart, (int)(e.y >> 8), e.w, nq, nq, hi,
+        entry_weights(g, pd, i0, j0, wt, cosr, g4, pstart, (int)(e.y >> 8), e.z, nq, nq, hi,
                       hi + (size_t)nq * SLOT_BYTES);
     }
 }
@@ -1217,7 +1223,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 TPROF_END(2);
             }
             const uint4 e = sm.Es[sv];
-            const uint32_t pstart = e.x, nk = e.y & 255, mask = e.z, blist = e.w;
+            const uint32_t pstart = e.x, nk = e.y & 255, mask = e.z;
             const int row = (int)(e.y >> 8);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -1247,7 +1253,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             TPROF_BEGIN;
             const int nq = (dbg & 1) ? 0 : __popc(mask);
             uint8_t* bst = &sm.B[sb * B_STAGE];
-            entry_weights(g, pd, i0, j0, wt, cosr, g4, pstart, row, blist, nq, MAXQ, bst, bst + B_HALF);
+            entry_weights(g, pd, i0, j0, wt, cosr, g4, pstart, row, mask, nq, MAXQ, bst, bst + B_HALF);
             if (wt == 0) sm.Bmask[sb] = mask;
             if (!(dbg & 128)) tc::fence_proxy_async_smem();
             __syncwarp();
