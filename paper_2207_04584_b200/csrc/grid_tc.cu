@@ -1410,12 +1410,12 @@ hegrid_status launch_accumulate_tc(const hegrid_plan_s* p, const float* d_v, int
     // candidate samples in L2: 34.4 GB per cfg4 launch against 38.1 GB with all 32 channel
     // blocks of a tile together and row-major tiles (75 GB tile-major, group 1).  On-the-fly
     // weights: tile-major.  Few channel blocks (cfg2, cfg3): row-major tiles, measured faster
-    // there.  The snake changes a tile's accumulation order, so it depends on the channel count
-    // only (both weight modes give bit-identical maps).  HEGRID_TC_GROUP / _SUPER / _SNAKE
-    // override.
+    // there.  The snake fixes a tile's accumulation order, so it is on for every launch (both
+    // weight modes, any channel count: the maps stay bit-identical across channel blockings;
+    // neutral in time for cfg2 / cfg3).  HEGRID_TC_GROUP / _SUPER / _SNAKE override.
     int cgroup = pw ? std::min(ncb, 8) : 1;
     if (const char* e = getenv("HEGRID_TC_GROUP")) cgroup = std::max(1, std::min(ncb, atoi(e)));
-    int super_ = pw && ncb >= 8 ? 3 : 1, snake = ncb >= 8 ? 1 : 0;
+    int super_ = pw && ncb >= 8 ? 3 : 1, snake = 1;
     if (const char* e = getenv("HEGRID_TC_SUPER")) super_ = std::max(1, atoi(e));
     if (const char* e = getenv("HEGRID_TC_SNAKE")) snake = atoi(e);
     NfBuf nf;
