@@ -93,7 +93,7 @@ static_assert(TC_KC == 32 || TC_KC == 64, "chunks of 32 or 64 samples");
 #define HG_TC_NBS (HG_TC_MAXQ > 8 ? 1 : 2)
 #endif
 #ifndef HG_TC_NV
-#define HG_TC_NV 3
+#define HG_TC_NV 2          // 3 measured no faster; its 16 KB go to the weight ring
 #endif
 #ifndef HG_TC_SEG
 #define HG_TC_SEG 8         // segment length for dense plans
@@ -156,7 +156,7 @@ constexpr int NBF = 16;
 // entry into a byte ring in shared memory (entries placed contiguously, wrapping to 0).
 constexpr uint32_t SLOT_BYTES = KA * ATOM_SLOT;      // one block, one half (hi or lo): 2 KB at K = 32
 #ifndef HG_TC_RING_KB
-#define HG_TC_RING_KB 74
+#define HG_TC_RING_KB 94    // as large as the budget allows: cfg4 12.95 / 12.60 ms, cfg3 3.97 / 3.69 ms at 74 / 90 KB
 #endif
 constexpr uint32_t RING = HG_TC_RING_KB * 1024;
 static_assert(RING >= MAXQ * 2 * SLOT_BYTES, "the ring holds the largest entry");
@@ -165,7 +165,6 @@ constexpr uint32_t REGION0 = RING > NBS * B_STAGE ? RING : NBS * B_STAGE;
 struct TcSmem {
     uint8_t B[REGION0];                   // OTF: NBS weight stages of B_STAGE; PW: the ring
     uint8_t Vs[NV][V_STAGE];
-    float4 Gs[NV][TC_KC];                 // the chunk's sample geometry (plan order)
     uint4 Es[NV];                         // the chunk's schedule entry (written by the V loader)
     uint32_t Bmask[NBF];                  // block mask of the chunk in each weight stage / ring entry
     uint32_t Boff[NBF];                   // PW: ring offset of the entry
@@ -175,12 +174,25 @@ struct TcSmem {
     uint64_t seg_done[2], seg_free[2];    // D buffer d: segment's MMAs complete / promoted
     uint64_t bar_done;
     uint32_t tmem_base;
-    uint32_t sink[TC_THREADS];            // dependency sink, one word per thread (see the B producers' release)
-    float Wt[TC_TW * TC_TH];              // the tile's W per cell (epilogue)
     alignas(16) float M[TC_M][T_LD];      // fp32 master sums [channel][cell] (padded rows)
 };
 
 static_assert(offsetof(TcSmem, B) == 0 && offsetof(TcSmem, Vs) % 1024 == 0, "stage layout");
+// Shared memory not worth its own bytes (the weight ring gets them; a larger ring measured
+// faster: cfg4 12.95 / 12.85 / 12.60 ms at 74 / 80 / 90 KB):
+//  * the chunk's sample geometry (on-the-fly mode only) lives behind the NBS weight stages in
+//    the region the ring occupies in the precomputed-weight mode;
+static_assert(NBS * B_STAGE + NV * TC_KC * sizeof(float4) <= REGION0, "geometry stages fit behind the B stages");
+__device__ __forceinline__ float4* geo_stage(TcSmem& sm, int sv) {
+    return reinterpret_cast<float4*>(sm.B + NBS * B_STAGE) + sv * TC_KC;
+}
+//  * the per-thread dependency sink (see the A producers' release) is the padding column of
+//    the master tile (columns TC_TW * TC_TH .. T_LD - 1 are never read);
+static_assert((T_LD - TC_TW * TC_TH) * TC_M >= TC_THREADS, "a sink word per thread in the master padding");
+__device__ __forceinline__ uint32_t* sink_word(TcSmem& sm, int tid) {
+    return reinterpret_cast<uint32_t*>(&sm.M[tid / (T_LD - TC_TW * TC_TH)][TC_TW * TC_TH + tid % (T_LD - TC_TW * TC_TH)]);
+}
+//  * the tile's W per cell for the epilogue is staged in the ring once every MMA has completed.
 static_assert(sizeof(TcSmem) + 1024 <= 232448, "shared memory budget");
 
 // byte offset of (slot q, cell n, sample quad kq) inside one half (hi or lo) of an operand
@@ -962,7 +974,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                     // the geometry feeds the on-the-fly B producers only
                     tc::mbar_arrive_expect_tx(&sm.v_full[sv], (uint32_t)V_STAGE + (PW ? 0u : nk * 16));
                     tc::tma_load_2d(&sm.Vs[sv][0], &tmap_v, cb, (int)e.x, &sm.v_full[sv]);
-                    if (!PW) tc::bulk_g2s(&sm.Gs[sv][0], pd.geo + e.x, nk * 16, &sm.v_full[sv]);
+                    if (!PW) tc::bulk_g2s(geo_stage(sm, sv), pd.geo + e.x, nk * 16, &sm.v_full[sv]);
                 }
             }
             __syncwarp();
@@ -1109,7 +1121,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const float lsum = s0 + s1;
             const uint32_t dep = ee.x ^ ee.y ^ ee.z ^ __float_as_uint(lsum);
             if (warp == 4 && lane == 0 && tl_on && c < 256) g_tl[c][8] = clock64() + (dep == 0x12345u);
-            asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[tid])), "r"(dep) : "memory");
+            asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(sink_word(sm, tid))), "r"(dep) : "memory");
             // one arrive per warp (hundreds of per-thread arrives on one mbarrier serialise)
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&sm.v_empty[sv]);
@@ -1227,7 +1239,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
             const int row = (int)(e.y >> 8);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                g4[u] = sm.Gs[sv][4 * kq + u];
+                g4[u] = geo_stage(sm, sv)[4 * kq + u];
                 if ((uint32_t)(4 * kq + u) >= nk) g4[u] = make_float4(0.0f, kInvalidDy, 0.0f, 0.0f);
             }
             // Release the value stage now.  An mbarrier arrive does not wait for this
@@ -1239,7 +1251,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 for (int u = 0; u < 4; ++u)
                     dep ^= __float_as_uint(g4[u].x) ^ __float_as_uint(g4[u].y) ^
                            __float_as_uint(g4[u].z) ^ __float_as_uint(g4[u].w);
-                asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(&sm.sink[tid])), "r"(dep) : "memory");
+                asm volatile("st.shared.u32 [%0], %1;" :: "r"(tc::smem_u32(sink_word(sm, tid))), "r"(dep) : "memory");
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&sm.v_empty[sv]);
             }
@@ -1274,7 +1286,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
     }
     if (tid < TC_TW * TC_TH) {
         const int i = i0 + tid % TC_TW, j = j0 + tid / TC_TW;
-        sm.Wt[tid] = (i < g.nx && j < g.ny) ? __ldg(&wsum[(int64_t)j * g.nx + i]) : 0.0f;
+        reinterpret_cast<float*>(sm.B)[tid] = (i < g.nx && j < g.ny) ? __ldg(&wsum[(int64_t)j * g.nx + i]) : 0.0f;
     }
     __syncthreads();
     {
@@ -1289,7 +1301,7 @@ k_accum_tc(const __grid_constant__ Geom g, const __grid_constant__ CUtensorMap t
                 if (nsplit > 1) {                      // partial sum of this part
                     part[((int64_t)sp * C + ch) * cells + (int64_t)j * g.nx + i] = S;
                 } else {
-                    const float W = sm.Wt[y * TC_TW + x];
+                    const float W = reinterpret_cast<const float*>(sm.B)[y * TC_TW + x];
                     out[(int64_t)ch * cells + (int64_t)j * g.nx + i] = W > 0.0f ? __fdiv_rn(S, W) : qnan;
                 }
             }
