@@ -25,7 +25,7 @@
 //                     the block rows r with r % NI == i: per run of consecutive in-reach
 //                     blocks, 4 K-steps x 2 MMAs (N = 16 r), one commit per chunk;
 //   warp 1          : value loader: one 2D TMA box (32 plan rows x 128 channels) per chunk
-//                     into a 3-stage ring (+ the chunk's geometry in on-the-fly mode);
+//                     into a 2-stage ring (+ the chunk's geometry in on-the-fly mode);
 //   warp 2 (PW)     : weight loader: the chunk's precomputed weight-image bytes into a ring;
 //   A producers     : (thread = channel = TMEM lane) split the staged values into the tf32
 //                     hi part and the packed bf16 correction operand and tcgen05.st them into
